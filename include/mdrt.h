@@ -1,0 +1,178 @@
+/*
+ * mdrt.h -- C ABI of the B200 multi-depth-camera renderer (libmdrt.so).
+ *
+ * The reference renderer (`multidepth`, /root/reference/pkg/src/multidepth) is a
+ * Python package whose operator/plugin seam is the backend registry
+ * `kernels.get_render_fn(name) -> render_batch(...)` (kernels/__init__.py:53-60).
+ * Every entry point below replaces one piece of that path; the cited
+ * file:line is the reference interface it stands in for. All pointers are
+ * plain host or device pointers with explicit sizes; there are no torch
+ * types in any signature. Functions return 0 on success and a negative
+ * MDRT_E* code on failure; mdrt_last_error() then holds a message
+ * (thread-local). Python raises ValueError for MDRT_EINVAL and RuntimeError
+ * otherwise, matching the reference's error behaviour (kernels/__init__.py:38-50,
+ * scene.py:228-250).
+ *
+ * Units/conventions follow the reference exactly: quaternions are (w,x,y,z);
+ * camera frame +z forward, +x right, +y down (camera.py:3-7); pixel centres at
+ * +0.5 (camera.py:83-84); output is Euclidean range in metres; a miss reads
+ * exactly float32(d_max) (scene.py:336-338).
+ */
+#ifndef MDRT_H
+#define MDRT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDRT_ABI_VERSION 1
+
+#define MDRT_OK 0
+#define MDRT_EINVAL -1   /* bad argument (shape/range/state)            */
+#define MDRT_ECUDA -2    /* CUDA runtime error (no device, launch, OOM) */
+#define MDRT_ESTATE -3   /* call out of order (e.g. render before commit) */
+
+/* flags for mdrt_step_args.flags */
+#define MDRT_EARLY_TERMINATION 0x1 /* bound each query by the best hit so far (numba_backend.py:191) */
+#define MDRT_SENSOR 0x2            /* fused noise/dropout/clamp epilogue (sensor.py:55-82)          */
+#define MDRT_LATENCY 0x4           /* fused latency ring write + delayed read (sensor.py:103-150)   */
+#define MDRT_COUNT 0x8             /* count BVH node visits / triangle tests into `counters`         */
+#define MDRT_NO_CULL 0x10          /* disable per-view link culling (debug / A-B parity)            */
+
+typedef struct mdrt_ctx mdrt_ctx;
+
+/* Per-context statistics (mdrt_get_stats). */
+typedef struct {
+    int64_t num_bodies;
+    int64_t body_triangles;
+    int64_t body_nodes;
+    int64_t terrain_triangles;
+    int64_t terrain_nodes;
+    int64_t terrain_depth;       /* max depth of the terrain tree (root = 0)           */
+    int64_t body_max_depth;      /* max depth over the link trees                      */
+    int64_t node_bytes;          /* device bytes of all BVH node records (64 B each)   */
+    int64_t tri_bytes;           /* device bytes of all triangle records (48 B each)   */
+    int64_t node_record_size;    /* 64                                                 */
+    int64_t tri_record_size;     /* 48                                                 */
+} mdrt_stats;
+
+/* One render step. Device pointers unless noted. Shapes use N = num_envs of
+ * this call (an env slice), B = bodies, C = cameras, H x W pixels. */
+typedef struct {
+    int32_t num_envs;          /* N (this slice)                                      */
+    int32_t flags;             /* MDRT_* flags                                        */
+    int64_t env_offset;        /* global index of env 0 of this slice (RNG counter)   */
+
+    /* body poses: replaces Scene.set_body_poses state (scene.py:235-250) */
+    const float *body_pos;     /* (N,B,3)                                             */
+    const float *body_rot;     /* (N,B,4) wxyz, any nonzero norm (normalised on device) */
+
+    /* per-(env,cam) randomisation: Scene.set_camera_randomization (scene.py:256-273) */
+    const float *cam_off_pos;  /* (N,C,3) or NULL                                     */
+    const float *cam_off_rot;  /* (N,C,4) or NULL                                     */
+    const float *fov_delta;    /* (N,C) degrees or NULL                               */
+
+    /* seam mode (render_batch, numba_backend.py:222): precomposed camera poses and
+     * per-pixel ray grids. When cam_pos != NULL the rig/body composition is skipped. */
+    const float *cam_pos;      /* (N,C,3) or NULL                                     */
+    const float *cam_rot;      /* (N,C,4) or NULL                                     */
+    const float *ray_dirs;     /* (RN,C,H,W,3) camera-frame dirs or NULL (intrinsics) */
+    const float *ray_scale;    /* (RN,C,H,W) |dir| or NULL                            */
+    int32_t ray_envs;          /* RN: 1 (shared) or N                                 */
+
+    /* sensor model: apply_noise_dropout (sensor.py:55-82) */
+    double noise_scale;
+    double dropout_p;
+    const double *fill;        /* HOST (C,) dropout fill per camera, NULL -> d_max    */
+    uint64_t sensor_key;       /* rng.stream_key(seed, "sensor") (rng.py:61-68)       */
+    int64_t step;              /* counter `step` of the sensor stream                 */
+
+    /* latency ring: FrameBuffer push + fetch_delayed_batch (sensor.py:103-150) */
+    float *ring;               /* (R,N,C,H,W)                                         */
+    int32_t ring_slots;        /* R                                                   */
+    int32_t write_slot;        /* slot receiving this step's frame                    */
+    int32_t ring_count;        /* K frames retained after this push (<= R, <= 32)     */
+    const double *ring_times;  /* HOST (K,) timestamps, oldest first (incl. this one) */
+    const int32_t *ring_order; /* HOST (K,) slot of each retained frame, oldest first */
+    double now;                /* fetch time                                          */
+    const double *delays;      /* (N,) per-env delay, device                          */
+    int32_t *read_slot;        /* (N,) scratch/out: selected slot per env, device      */
+
+    float *out_clean;          /* (N,C,H,W) clean range depth, or NULL                */
+    float *out;                /* (N,C,H,W) final output (sensor/latency applied)     */
+    unsigned long long *counters; /* (2,) device [node visits, triangle tests] or NULL */
+} mdrt_step_args;
+
+/* ---- library ---------------------------------------------------------- */
+int mdrt_abi_version(void);
+const char *mdrt_last_error(void);
+/* number of visible CUDA devices (0 on a host without a GPU) */
+int mdrt_device_count(int32_t *count);
+
+/* ---- context: replaces Scene geometry state (scene.py:159-211) --------- */
+int mdrt_create(int32_t device, mdrt_ctx **out);
+int mdrt_destroy(mdrt_ctx *ctx);
+
+/* Register a body (link) mesh in its local frame; SAH BVH built once on the
+ * host. Replaces Body/build_bvh (scene.py:165-176, bvh.py:68-136). Triangles
+ * with area < 1e-12 are expected to be removed by the caller (mesh.py:47-56). */
+int mdrt_add_body(mdrt_ctx *ctx, const double *verts, int64_t nv, const int64_t *faces,
+                  int64_t nf, int32_t *body_id);
+/* Set the static world-frame terrain mesh (scene.py:191-196). */
+int mdrt_set_terrain(mdrt_ctx *ctx, const double *verts, int64_t nv, const int64_t *faces,
+                     int64_t nf);
+/* Camera rig: CameraModel (camera.py:20-65) x C. parent[c] = body index or -1
+ * (mount is a world pose, scene.py:286-287). mount_rot (C,4) wxyz. HOST arrays. */
+int mdrt_set_cameras(mdrt_ctx *ctx, int32_t C, int32_t W, int32_t H, const double *hfov_deg,
+                     const double *vfov_deg, const double *d_max, const int32_t *parent,
+                     const double *mount_pos, const double *mount_rot);
+/* Upload all geometry to the device; geometry is immutable afterwards
+ * (test_render.py:252-265 "BVHs never rebuilt"). */
+int mdrt_commit(mdrt_ctx *ctx);
+int mdrt_get_stats(mdrt_ctx *ctx, mdrt_stats *out);
+
+/* ---- per step ----------------------------------------------------------
+ * Replaces render() (scene.py:332-348) -> render_batch (numba_backend.py:222-234)
+ * and, with MDRT_SENSOR / MDRT_LATENCY, the sensor stage apply_noise_dropout
+ * (sensor.py:55-82) and FrameBuffer push/fetch_delayed_batch (sensor.py:122-150),
+ * fused into one traversal kernel. `stream` is a cudaStream_t (NULL = default). */
+int mdrt_render(mdrt_ctx *ctx, const mdrt_step_args *args, void *stream);
+
+/* Standalone sensor epilogue on an existing (N,C,H,W) depth tensor
+ * (apply_noise_dropout, sensor.py:55-82). d_max/fill: HOST (C,). */
+int mdrt_noise_dropout(const float *depth, float *out, int32_t N, int32_t C, int32_t H,
+                       int32_t W, int64_t env_offset, const double *d_max, const double *fill,
+                       double noise_scale, double dropout_p, uint64_t key, int64_t step,
+                       void *stream);
+
+/* FrameBuffer.fetch_delayed_batch gather (sensor.py:141-150): out[e] = frames[slot[e]][e].
+ * frames: R device pointers packed in a HOST array; slot: (N,) device. */
+int mdrt_gather_delayed(const float *const *frames, int32_t R, const int32_t *slot, float *out,
+                        int64_t N, int64_t frame_elems_per_env, void *stream);
+
+/* Per-env slot selection on device (sensor.py:138-139): slot[e] = order[max(bisect_right(
+ * times, now - delays[e]) - 1, 0)]. times/order: HOST (K,), K <= 32. */
+int mdrt_select_slots(const double *times, const int32_t *order, int32_t K, double now,
+                      const double *delays, int32_t *slot, int64_t N, void *stream);
+
+/* downsample_min (sensor.py:85-100): block minimum over trailing (H,W). */
+int mdrt_downsample_min(const float *in, float *out, int64_t planes, int32_t H, int32_t W,
+                        int32_t factor, void *stream);
+
+/* Host-only BVH check (no device needed): builds the packed tree for one mesh
+ * exactly as mdrt_add_body/mdrt_set_terrain do and verifies its invariants
+ * (every triangle in exactly one leaf, child boxes enclose their triangles,
+ * depth <= 32). Fills info = {nodes, triangles, depth, leaves}. Returns
+ * MDRT_EINVAL with a message when an invariant fails. */
+int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_t nf,
+                   int64_t info[4]);
+
+/* Synchronise the context's device (debug/tests). */
+int mdrt_sync(mdrt_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDRT_H */

@@ -1,0 +1,225 @@
+"""ctypes binding of libmdrt.so (C ABI in include/mdrt.h).
+
+There is no fallback: if the library is missing or no CUDA device is visible
+every entry point raises. The library is loaded from this package directory
+(built in-tree by ``paper_2602_03002_b200.build``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmdrt.so")
+
+MDRT_OK = 0
+MDRT_EINVAL = -1
+MDRT_ECUDA = -2
+MDRT_ESTATE = -3
+
+EARLY_TERMINATION = 0x1
+SENSOR = 0x2
+LATENCY = 0x4
+COUNT = 0x8
+NO_CULL = 0x10
+
+_c_dp = ctypes.POINTER(ctypes.c_double)
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "num_bodies", "body_triangles", "body_nodes", "terrain_triangles", "terrain_nodes",
+        "terrain_depth", "body_max_depth", "node_bytes", "tri_bytes", "node_record_size",
+        "tri_record_size")]
+
+    def as_dict(self) -> dict:
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class StepArgs(ctypes.Structure):
+    _fields_ = [
+        ("num_envs", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("env_offset", ctypes.c_int64),
+        ("body_pos", ctypes.c_void_p),
+        ("body_rot", ctypes.c_void_p),
+        ("cam_off_pos", ctypes.c_void_p),
+        ("cam_off_rot", ctypes.c_void_p),
+        ("fov_delta", ctypes.c_void_p),
+        ("cam_pos", ctypes.c_void_p),
+        ("cam_rot", ctypes.c_void_p),
+        ("ray_dirs", ctypes.c_void_p),
+        ("ray_scale", ctypes.c_void_p),
+        ("ray_envs", ctypes.c_int32),
+        ("noise_scale", ctypes.c_double),
+        ("dropout_p", ctypes.c_double),
+        ("fill", _c_dp),
+        ("sensor_key", ctypes.c_uint64),
+        ("step", ctypes.c_int64),
+        ("ring", ctypes.c_void_p),
+        ("ring_slots", ctypes.c_int32),
+        ("write_slot", ctypes.c_int32),
+        ("ring_count", ctypes.c_int32),
+        ("ring_times", _c_dp),
+        ("ring_order", _c_i32p),
+        ("now", ctypes.c_double),
+        ("delays", ctypes.c_void_p),
+        ("read_slot", ctypes.c_void_p),
+        ("out_clean", ctypes.c_void_p),
+        ("out", ctypes.c_void_p),
+        ("counters", ctypes.c_void_p),
+    ]
+
+
+class MdrtError(RuntimeError):
+    pass
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libmdrt.so (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2602_03002_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        sig = {
+            "mdrt_abi_version": (ctypes.c_int, []),
+            "mdrt_last_error": (ctypes.c_char_p, []),
+            "mdrt_device_count": (ctypes.c_int, [_c_i32p]),
+            "mdrt_create": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(vp)]),
+            "mdrt_destroy": (ctypes.c_int, [vp]),
+            "mdrt_add_body": (ctypes.c_int, [vp, _c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64, _c_i32p]),
+            "mdrt_set_terrain": (ctypes.c_int, [vp, _c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64]),
+            "mdrt_set_cameras": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _c_dp,
+                                                _c_dp, _c_dp, _c_i32p, _c_dp, _c_dp]),
+            "mdrt_commit": (ctypes.c_int, [vp]),
+            "mdrt_get_stats": (ctypes.c_int, [vp, ctypes.POINTER(Stats)]),
+            "mdrt_render": (ctypes.c_int, [vp, ctypes.POINTER(StepArgs), vp]),
+            "mdrt_noise_dropout": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.c_int32, ctypes.c_int64, _c_dp, _c_dp,
+                                                  ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                                                  ctypes.c_int64, vp]),
+            "mdrt_gather_delayed": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_int32, vp, vp,
+                                                   ctypes.c_int64, ctypes.c_int64, vp]),
+            "mdrt_select_slots": (ctypes.c_int, [_c_dp, _c_i32p, ctypes.c_int32, ctypes.c_double, vp, vp,
+                                                 ctypes.c_int64, vp]),
+            "mdrt_downsample_min": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                                   ctypes.c_int32, vp]),
+            "mdrt_bvh_check": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64, _c_i64p]),
+            "mdrt_sync": (ctypes.c_int, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return _lib
+
+
+# symbols declared by include/mdrt.h (checked by tests/test_abi.py)
+EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_create", "mdrt_destroy",
+           "mdrt_add_body", "mdrt_set_terrain", "mdrt_set_cameras", "mdrt_commit", "mdrt_get_stats",
+           "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
+           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_sync")
+
+
+def check(rc: int) -> None:
+    if rc == MDRT_OK:
+        return
+    msg = lib().mdrt_last_error().decode("utf-8", "replace")
+    if rc == MDRT_EINVAL:
+        raise ValueError(msg)
+    raise MdrtError(f"mdrt error {rc}: {msg}")
+
+
+def device_count() -> int:
+    n = ctypes.c_int32(0)
+    check(lib().mdrt_device_count(ctypes.byref(n)))
+    return int(n.value)
+
+
+def dptr(a) -> ctypes.Array:
+    return a.ctypes.data_as(_c_dp)
+
+
+def bvh_check(verts, faces) -> dict:
+    """Host-only build + invariant check of one mesh's packed BVH (no GPU needed)."""
+    import numpy as np
+    v = np.ascontiguousarray(verts, dtype=np.float64)
+    f = np.ascontiguousarray(faces, dtype=np.int64)
+    info = np.zeros(4, np.int64)
+    check(lib().mdrt_bvh_check(dptr(v), len(v), f.ctypes.data_as(_c_i64p), len(f),
+                               info.ctypes.data_as(_c_i64p)))
+    return dict(nodes=int(info[0]), triangles=int(info[1]), depth=int(info[2]), leaves=int(info[3]))
+
+
+class Context:
+    """Owns one mdrt_ctx (geometry + camera rig on one device)."""
+
+    def __init__(self, device: int):
+        self._ptr = ctypes.c_void_p()
+        check(lib().mdrt_create(int(device), ctypes.byref(self._ptr)))
+        self.device = int(device)
+
+    def __del__(self):
+        ptr = getattr(self, "_ptr", None)
+        if ptr and ptr.value and _lib is not None:
+            _lib.mdrt_destroy(ptr)
+            self._ptr = ctypes.c_void_p()
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def add_body(self, verts, faces) -> int:
+        import numpy as np
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        f = np.ascontiguousarray(faces, dtype=np.int64)
+        bid = ctypes.c_int32(-1)
+        check(lib().mdrt_add_body(self._ptr, dptr(v), len(v), f.ctypes.data_as(_c_i64p), len(f),
+                                  ctypes.byref(bid)))
+        return int(bid.value)
+
+    def set_terrain(self, verts, faces) -> None:
+        import numpy as np
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        f = np.ascontiguousarray(faces, dtype=np.int64)
+        check(lib().mdrt_set_terrain(self._ptr, dptr(v), len(v), f.ctypes.data_as(_c_i64p), len(f)))
+
+    def set_cameras(self, width, height, hfov, vfov, d_max, parent, mount_pos, mount_rot) -> None:
+        import numpy as np
+        hf = np.ascontiguousarray(hfov, np.float64)
+        vf = np.ascontiguousarray(vfov, np.float64)
+        dm = np.ascontiguousarray(d_max, np.float64)
+        pa = np.ascontiguousarray(parent, np.int32)
+        mp = np.ascontiguousarray(mount_pos, np.float64)
+        mr = np.ascontiguousarray(mount_rot, np.float64)
+        check(lib().mdrt_set_cameras(self._ptr, len(hf), int(width), int(height), dptr(hf), dptr(vf),
+                                     dptr(dm), pa.ctypes.data_as(_c_i32p), dptr(mp), dptr(mr)))
+
+    def commit(self) -> None:
+        check(lib().mdrt_commit(self._ptr))
+
+    def stats(self) -> dict:
+        s = Stats()
+        check(lib().mdrt_get_stats(self._ptr, ctypes.byref(s)))
+        return s.as_dict()
+
+    def render(self, args: StepArgs, stream: int) -> None:
+        check(lib().mdrt_render(self._ptr, ctypes.byref(args), ctypes.c_void_p(stream)))
+
+    def sync(self) -> None:
+        check(lib().mdrt_sync(self._ptr))

@@ -1,0 +1,538 @@
+// C ABI of libmdrt.so (declared in include/mdrt.h).
+//
+// Host-side ownership mirrors the reference Scene (scene.py:150-211): geometry
+// is registered, built once (SAH BVH per mesh, bvh_build.cpp) and committed to
+// the device; afterwards only per-step pose/camera/sensor data flows in.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <limits>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mdrt.h"
+#include "bvh_build.h"
+#include "mdrt_kernels.h"
+
+using namespace mdrt;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ArgError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw CudaError(std::string(#expr) + ": " + cudaGetErrorName(e_) + " (" +             \
+                            cudaGetErrorString(e_) + ")");                                         \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return MDRT_OK;
+    } catch (const ArgError& e) {
+        g_err = e.what();
+        return MDRT_EINVAL;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return MDRT_EINVAL;
+    } catch (const StateError& e) {
+        g_err = e.what();
+        return MDRT_ESTATE;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return MDRT_ECUDA;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return MDRT_ECUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MDRT_ECUDA;
+    }
+}
+
+void need(bool ok, const char* msg) {
+    if (!ok) throw ArgError(msg);
+}
+
+template <class T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;  // elements
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        CK(cudaMalloc(&ptr, n * sizeof(T)));
+        cap = n;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct mdrt_ctx {
+    int device = 0;
+    std::vector<PackedTree> bodies;
+    PackedTree terrain;
+    bool has_terrain = false;
+    // cameras
+    int32_t C = 0, W = 0, H = 0;
+    std::vector<CamRig> rigs;
+    bool committed = false;
+    // device geometry
+    DevBuf<PackedNode> nodes;
+    DevBuf<PackedTri> tris;
+    DevBuf<BodyInfo> body_info;
+    DevBuf<CamRig> rig_buf;
+    int32_t terrain_root = -1;
+    mdrt_stats stats{};
+    // per-step scratch
+    DevBuf<ViewRec> views;
+    DevBuf<LinkRec> links;
+
+    void use_device() const { CK(cudaSetDevice(device)); }
+};
+
+extern "C" {
+
+int mdrt_abi_version(void) { return MDRT_ABI_VERSION; }
+
+const char* mdrt_last_error(void) { return g_err.c_str(); }
+
+int mdrt_device_count(int32_t* count) {
+    return guarded([&] {
+        need(count != nullptr, "count is NULL");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            n = 0;
+        }
+        *count = n;
+    });
+}
+
+int mdrt_create(int32_t device, mdrt_ctx** out) {
+    return guarded([&] {
+        need(out != nullptr, "out is NULL");
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        need(device >= 0 && device < n, "device index out of range");
+        auto* ctx = new mdrt_ctx();
+        ctx->device = device;
+        *out = ctx;
+    });
+}
+
+int mdrt_destroy(mdrt_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        ctx->nodes.release();
+        ctx->tris.release();
+        ctx->body_info.release();
+        ctx->rig_buf.release();
+        ctx->views.release();
+        ctx->links.release();
+        delete ctx;
+    });
+}
+
+int mdrt_add_body(mdrt_ctx* ctx, const double* verts, int64_t nv, const int64_t* faces, int64_t nf,
+                  int32_t* body_id) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        if (ctx->committed) throw StateError("geometry is immutable after mdrt_commit");
+        need(verts && faces && nv > 0, "body mesh arrays are empty");
+        need(nf > 0, "body has no triangles");
+        ctx->bodies.push_back(build_tree(verts, nv, faces, nf));
+        if (body_id) *body_id = static_cast<int32_t>(ctx->bodies.size() - 1);
+    });
+}
+
+int mdrt_set_terrain(mdrt_ctx* ctx, const double* verts, int64_t nv, const int64_t* faces, int64_t nf) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        if (ctx->committed) throw StateError("geometry is immutable after mdrt_commit");
+        need(verts && faces && nv > 0, "terrain mesh arrays are empty");
+        need(nf > 0, "terrain mesh has no triangles");
+        ctx->terrain = build_tree(verts, nv, faces, nf);
+        ctx->has_terrain = true;
+    });
+}
+
+int mdrt_set_cameras(mdrt_ctx* ctx, int32_t C, int32_t W, int32_t H, const double* hfov_deg,
+                     const double* vfov_deg, const double* d_max, const int32_t* parent,
+                     const double* mount_pos, const double* mount_rot) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        if (ctx->committed) throw StateError("cameras are immutable after mdrt_commit");
+        need(C >= 1 && C <= 64, "camera count must be in [1, 64]");
+        need(W >= 1 && H >= 1 && W <= 32767 && H <= 32767, "bad image size");
+        need(hfov_deg && vfov_deg && d_max && parent && mount_pos && mount_rot, "NULL camera array");
+        ctx->C = C;
+        ctx->W = W;
+        ctx->H = H;
+        ctx->rigs.assign(C, CamRig{});
+        for (int c = 0; c < C; ++c) {
+            CamRig& r = ctx->rigs[c];
+            need(hfov_deg[c] > 0 && hfov_deg[c] < 180 && vfov_deg[c] > 0 && vfov_deg[c] < 180,
+                 "fov must be in (0, 180) degrees");
+            need(d_max[c] > 0, "d_max must be positive");
+            for (int a = 0; a < 3; ++a) r.mount_pos[a] = mount_pos[c * 3 + a];
+            for (int a = 0; a < 4; ++a) r.mount_rot[a] = mount_rot[c * 4 + a];
+            r.hfov_deg = hfov_deg[c];
+            r.vfov_deg = vfov_deg[c];
+            r.d_max = d_max[c];
+            r.parent = parent[c];
+        }
+    });
+}
+
+int mdrt_commit(mdrt_ctx* ctx) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        if (ctx->committed) throw StateError("already committed");
+        if (ctx->C < 1) throw StateError("mdrt_set_cameras must precede mdrt_commit");
+        const int B = static_cast<int>(ctx->bodies.size());
+        for (int c = 0; c < ctx->C; ++c)
+            need(ctx->rigs[c].parent >= -1 && ctx->rigs[c].parent < B, "camera parent_body out of range");
+        ctx->use_device();
+        // concatenate: terrain first, then bodies
+        std::vector<PackedNode> nodes;
+        std::vector<PackedTri> tris;
+        std::vector<BodyInfo> infos;
+        mdrt_stats st{};
+        auto append = [&](PackedTree& t) -> int32_t {
+            const int32_t noff = static_cast<int32_t>(nodes.size());
+            const int32_t toff = static_cast<int32_t>(tris.size());
+            if (static_cast<int64_t>(tris.size()) + static_cast<int64_t>(t.tris.size()) >= (int64_t(1) << 27))
+                throw ArgError("too many triangles (limit 2^27)");
+            offset_tree(t, noff, toff);
+            nodes.insert(nodes.end(), t.nodes.begin(), t.nodes.end());
+            tris.insert(tris.end(), t.tris.begin(), t.tris.end());
+            offset_tree(t, -noff, -toff);  // keep the host copy relative
+            return noff;
+        };
+        if (ctx->has_terrain) {
+            ctx->terrain_root = append(ctx->terrain);
+            st.terrain_nodes = static_cast<int64_t>(ctx->terrain.nodes.size());
+            st.terrain_triangles = static_cast<int64_t>(ctx->terrain.tris.size());
+            st.terrain_depth = ctx->terrain.depth;
+        }
+        for (auto& b : ctx->bodies) {
+            BodyInfo bi{};
+            bi.root = append(b);
+            bi.cx = static_cast<float>(b.center[0]);
+            bi.cy = static_cast<float>(b.center[1]);
+            bi.cz = static_cast<float>(b.center[2]);
+            bi.r = static_cast<float>(b.radius * (1.0 + 1e-6)) + 1e-5f;
+            infos.push_back(bi);
+            st.body_nodes += static_cast<int64_t>(b.nodes.size());
+            st.body_triangles += static_cast<int64_t>(b.tris.size());
+            st.body_max_depth = std::max<int64_t>(st.body_max_depth, b.depth);
+        }
+        st.num_bodies = B;
+        st.node_record_size = sizeof(PackedNode);
+        st.tri_record_size = sizeof(PackedTri);
+        st.node_bytes = static_cast<int64_t>(nodes.size() * sizeof(PackedNode));
+        st.tri_bytes = static_cast<int64_t>(tris.size() * sizeof(PackedTri));
+        if (nodes.empty()) nodes.push_back(PackedNode{});
+        if (tris.empty()) tris.push_back(PackedTri{});
+        if (infos.empty()) infos.push_back(BodyInfo{});
+        ctx->nodes.reserve(nodes.size());
+        ctx->tris.reserve(tris.size());
+        ctx->body_info.reserve(infos.size());
+        ctx->rig_buf.reserve(ctx->rigs.size());
+        CK(cudaMemcpy(ctx->nodes.ptr, nodes.data(), nodes.size() * sizeof(PackedNode), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->tris.ptr, tris.data(), tris.size() * sizeof(PackedTri), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->body_info.ptr, infos.data(), infos.size() * sizeof(BodyInfo), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->rig_buf.ptr, ctx->rigs.data(), ctx->rigs.size() * sizeof(CamRig),
+                      cudaMemcpyHostToDevice));
+        ctx->stats = st;
+        ctx->committed = true;
+    });
+}
+
+int mdrt_get_stats(mdrt_ctx* ctx, mdrt_stats* out) {
+    return guarded([&] {
+        need(ctx && out, "NULL argument");
+        if (!ctx->committed) throw StateError("mdrt_commit first");
+        *out = ctx->stats;
+    });
+}
+
+int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
+    return guarded([&] {
+        need(ctx && a, "NULL argument");
+        if (!ctx->committed) throw StateError("mdrt_commit must precede mdrt_render");
+        const int32_t N = a->num_envs, C = ctx->C, B = static_cast<int32_t>(ctx->bodies.size());
+        need(N >= 1, "num_envs must be >= 1");
+        need(a->out != nullptr, "out is NULL");
+        const bool seam = a->cam_pos != nullptr;
+        need(!seam || a->cam_rot != nullptr, "cam_rot is NULL while cam_pos is set");
+        need(B == 0 || (a->body_pos && a->body_rot), "body poses are NULL");
+        need(!(a->cam_off_pos || a->cam_off_rot) || (a->cam_off_pos && a->cam_off_rot),
+             "cam_off_pos and cam_off_rot must be given together");
+        need(!a->ray_dirs || a->ray_scale, "ray_scale is NULL while ray_dirs is set");
+        need(!a->ray_dirs || a->ray_envs == 1 || a->ray_envs == N, "ray_envs must be 1 or num_envs");
+        const bool sensor = (a->flags & MDRT_SENSOR) != 0;
+        const bool latency = (a->flags & MDRT_LATENCY) != 0;
+        if (sensor) {
+            need(a->noise_scale >= 0, "noise_scale must be >= 0");
+            need(a->dropout_p >= 0 && a->dropout_p < 1, "dropout_p must be in [0, 1)");
+        }
+        if (latency) {
+            need(a->ring && a->ring_slots >= 1 && a->ring_slots <= 32, "ring must have 1..32 slots");
+            need(a->write_slot >= 0 && a->write_slot < a->ring_slots, "write_slot out of range");
+            need(a->ring_count >= 1 && a->ring_count <= a->ring_slots, "ring_count out of range");
+            need(a->ring_times && a->ring_order && a->delays, "latency arrays are NULL");
+        }
+        need(!(a->flags & MDRT_COUNT) || a->counters, "counters is NULL with MDRT_COUNT");
+        ctx->use_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t nviews = static_cast<size_t>(N) * C;
+        ctx->views.reserve(nviews);
+        ctx->links.reserve(std::max<size_t>(1, nviews * std::max(B, 1)));
+
+        PrologueParams pp{};
+        pp.N = N; pp.C = C; pp.B = B; pp.W = ctx->W; pp.H = ctx->H;
+        pp.env_offset = a->env_offset;
+        pp.rigs = ctx->rig_buf.ptr;
+        pp.bodies = ctx->body_info.ptr;
+        pp.body_pos = a->body_pos;
+        pp.body_rot = a->body_rot;
+        pp.off_pos = seam ? nullptr : a->cam_off_pos;
+        pp.off_rot = seam ? nullptr : a->cam_off_rot;
+        pp.fov_delta = a->ray_dirs ? nullptr : a->fov_delta;
+        pp.cam_pos = a->cam_pos;
+        pp.cam_rot = a->cam_rot;
+        pp.grid_mode = a->ray_dirs != nullptr;
+        pp.no_cull = (a->flags & MDRT_NO_CULL) != 0;
+        unsigned long long key = a->sensor_key;
+        unsigned long long st = static_cast<unsigned long long>(a->step);
+        pp.hu_step = absorb(absorb(key, 0ULL), st);
+        pp.hn_step = absorb(absorb(key, 1ULL), st);
+        pp.latency = latency;
+        if (latency) {
+            pp.ring_count = a->ring_count;
+            pp.write_slot = a->write_slot;
+            pp.now = a->now;
+            pp.delays = a->delays;
+            for (int k = 0; k < a->ring_count; ++k) {
+                pp.ring_times[k] = a->ring_times[k];
+                need(a->ring_order[k] >= 0 && a->ring_order[k] < a->ring_slots, "ring_order out of range");
+                pp.ring_order[k] = a->ring_order[k];
+            }
+            pp.read_slot_out = a->read_slot;
+        }
+        pp.views = ctx->views.ptr;
+        pp.links = ctx->links.ptr;
+        launch_prologue(pp, static_cast<int64_t>(nviews), s);
+        CK(cudaGetLastError());
+
+        RenderParams rp{};
+        rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
+        rp.tiles_x = (ctx->W + kTileW - 1) / kTileW;
+        rp.tiles_per_view = rp.tiles_x * ((ctx->H + kTileH - 1) / kTileH);
+        rp.early_termination = (a->flags & MDRT_EARLY_TERMINATION) != 0;
+        rp.terrain_root = ctx->has_terrain ? ctx->terrain_root : -1;
+        rp.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);
+        rp.tris = reinterpret_cast<const float4*>(ctx->tris.ptr);
+        rp.views = ctx->views.ptr;
+        rp.links = ctx->links.ptr;
+        rp.ray_dirs = a->ray_dirs;
+        rp.ray_scale = a->ray_scale;
+        rp.ray_envs = a->ray_envs;
+        rp.sensor = sensor;
+        rp.noise_scale = a->noise_scale;
+        rp.dropout_p = a->dropout_p;
+        for (int c = 0; c < C; ++c) {
+            rp.dmax64[c] = ctx->rigs[c].d_max;
+            rp.fill[c] = a->fill ? a->fill[c] : ctx->rigs[c].d_max;
+        }
+        rp.ring = latency ? a->ring : nullptr;
+        rp.write_slot = a->write_slot;
+        rp.out_clean = a->out_clean;
+        rp.out = a->out;
+        rp.counters = a->counters;
+        const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;
+        need((warps * 32 + kBlock - 1) / kBlock < (int64_t(1) << 31), "launch too large");
+        launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, s);
+        CK(cudaGetLastError());
+    });
+}
+
+int mdrt_noise_dropout(const float* depth, float* out, int32_t N, int32_t C, int32_t H, int32_t W,
+                       int64_t env_offset, const double* d_max, const double* fill, double noise_scale,
+                       double dropout_p, uint64_t key, int64_t step, void* stream) {
+    return guarded([&] {
+        need(depth && out && d_max, "NULL argument");
+        need(N >= 0 && C >= 1 && C <= 64 && H >= 1 && W >= 1, "bad shape");
+        need(noise_scale >= 0, "noise_scale must be >= 0");
+        need(dropout_p >= 0 && dropout_p < 1, "dropout_p must be in [0, 1)");
+        NoiseParams p{};
+        p.in = depth;
+        p.out = out;
+        p.N = N; p.C = C; p.H = H; p.W = W;
+        p.env_offset = env_offset;
+        p.hu_step = absorb(absorb(key, 0ULL), static_cast<unsigned long long>(step));
+        p.hn_step = absorb(absorb(key, 1ULL), static_cast<unsigned long long>(step));
+        p.noise_scale = noise_scale;
+        p.dropout_p = dropout_p;
+        for (int c = 0; c < C; ++c) {
+            p.dmax[c] = d_max[c];
+            p.fill[c] = fill ? fill[c] : d_max[c];
+        }
+        const int64_t total = static_cast<int64_t>(N) * C * H * W;
+        if (total == 0) return;
+        launch_noise(p, total, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int mdrt_gather_delayed(const float* const* frames, int32_t R, const int32_t* slot, float* out, int64_t N,
+                        int64_t per_env, void* stream) {
+    return guarded([&] {
+        need(frames && slot && out, "NULL argument");
+        need(R >= 1 && R <= 32, "1..32 frames");
+        GatherParams p{};
+        for (int i = 0; i < R; ++i) p.frames[i] = frames[i];
+        p.slot = slot;
+        p.out = out;
+        p.N = N;
+        p.per_env = per_env;
+        const int64_t total = N * per_env;
+        if (total == 0) return;
+        launch_gather(p, total, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int mdrt_select_slots(const double* times, const int32_t* order, int32_t K, double now, const double* delays,
+                      int32_t* slot, int64_t N, void* stream) {
+    return guarded([&] {
+        need(times && order && delays && slot, "NULL argument");
+        need(K >= 1 && K <= 32, "K must be in [1, 32]");
+        SelectParams p{};
+        for (int k = 0; k < K; ++k) {
+            p.times[k] = times[k];
+            p.order[k] = order[k];
+        }
+        p.K = K;
+        p.now = now;
+        p.delays = delays;
+        p.slot = slot;
+        p.N = N;
+        if (N == 0) return;
+        launch_select(p, N, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int mdrt_downsample_min(const float* in, float* out, int64_t planes, int32_t H, int32_t W, int32_t factor,
+                        void* stream) {
+    return guarded([&] {
+        need(in && out, "NULL argument");
+        need(factor >= 1, "factor must be >= 1");
+        need(H % factor == 0 && W % factor == 0, "resolution not divisible by downsample factor");
+        DownsampleParams p{};
+        p.in = in;
+        p.out = out;
+        p.planes = planes;
+        p.H = H;
+        p.W = W;
+        p.f = factor;
+        const int64_t total = planes * (H / factor) * (W / factor);
+        if (total == 0) return;
+        launch_downsample(p, total, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int mdrt_bvh_check(const double* verts, int64_t nv, const int64_t* faces, int64_t nf, int64_t info[4]) {
+    return guarded([&] {
+        need(verts && faces && info, "NULL argument");
+        PackedTree t = build_tree(verts, nv, faces, nf);
+        std::vector<int> seen(t.tris.size(), 0);
+        int64_t leaves = 0;
+        int maxd = 0;
+        // walk: (ref, depth, box of this ref as stored in the parent)
+        struct It { int32_t ref; int depth; float lo[3], hi[3]; };
+        std::vector<It> st;
+        const float inf = std::numeric_limits<float>::infinity();
+        st.push_back({0, 0, {-inf, -inf, -inf}, {inf, inf, inf}});
+        while (!st.empty()) {
+            It it = st.back();
+            st.pop_back();
+            maxd = std::max(maxd, it.depth);
+            if (it.ref >= 0) {
+                need(it.ref < static_cast<int32_t>(t.nodes.size()), "node ref out of range");
+                const PackedNode& n = t.nodes[it.ref];
+                It a{n.ref0, it.depth + 1, {n.c0x0, n.c0y0, n.c0z0}, {n.c0x1, n.c0y1, n.c0z1}};
+                It b{n.ref1, it.depth + 1, {n.c1x0, n.c1y0, n.c1z0}, {n.c1x1, n.c1y1, n.c1z1}};
+                for (const It* c : {&a, &b}) {
+                    if (c->lo[0] > c->hi[0]) continue;  // empty child (single-leaf root)
+                    for (int k = 0; k < 3; ++k)
+                        need(c->lo[k] >= it.lo[k] && c->hi[k] <= it.hi[k], "child box escapes parent box");
+                    st.push_back(*c);
+                }
+            } else {
+                const int32_t v = ~it.ref;
+                const int64_t first = v >> 3, cnt = (v & 7) + 1;
+                need(cnt <= kMaxLeafTris, "leaf larger than kMaxLeafTris");
+                need(first + cnt <= static_cast<int64_t>(t.tris.size()), "leaf range out of bounds");
+                ++leaves;
+                for (int64_t i = first; i < first + cnt; ++i) {
+                    need(seen[i] == 0, "triangle referenced by two leaves");
+                    seen[i] = 1;
+                    const int64_t f = t.tri_index[i];
+                    for (int k = 0; k < 3; ++k) {
+                        const double* p = verts + faces[f * 3 + k] * 3;
+                        for (int a2 = 0; a2 < 3; ++a2)
+                            need(p[a2] >= it.lo[a2] && p[a2] <= it.hi[a2], "triangle escapes its leaf box");
+                    }
+                }
+            }
+        }
+        for (int x : seen) need(x == 1, "triangle not referenced by any leaf");
+        need(maxd <= kMaxDepth, "tree deeper than the traversal stack");
+        info[0] = static_cast<int64_t>(t.nodes.size());
+        info[1] = static_cast<int64_t>(t.tris.size());
+        info[2] = maxd;
+        info[3] = leaves;
+    });
+}
+
+int mdrt_sync(mdrt_ctx* ctx) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        ctx->use_device();
+        CK(cudaDeviceSynchronize());
+    });
+}
+
+}  // extern "C"

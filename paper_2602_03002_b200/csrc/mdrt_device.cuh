@@ -1,0 +1,209 @@
+// Device-side records and inline functions of the B200 renderer.
+//
+// Reference semantics restated here (paths under /root/reference/pkg/src/multidepth):
+//   trace()        -> _closest_hit/_slab_hit/_tri_t, kernels/numba_backend.py:37-152
+//   rng_*          -> rng.py:30-99 (splitmix64 absorb chain, bit-exact)
+//   sensor_apply() -> sensor.py:55-82 (noise, dropout, clamp; f64 like the reference)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mdrt {
+
+constexpr int kStack = 32;          // == kMaxDepth of the builder
+constexpr int kBlock = 128;         // threads per render block (4 warps, 4 tiles)
+constexpr int kTileW = 8;           // a warp renders an 8x4 pixel tile of one view
+constexpr int kTileH = 4;
+constexpr int kExit = INT32_MIN;    // traversal stack sentinel
+constexpr float kRayEps = 1e-6f;    // RAY_EPSILON (bvh.py:30): hits need t > 1e-6
+constexpr float kBaryEps = 1e-5f;   // fp32 watertightness margin on barycentrics
+
+// Per-camera rig constants (CameraModel, camera.py:20-65), uploaded at commit.
+struct CamRig {
+    double mount_pos[3];
+    double mount_rot[4];
+    double hfov_deg, vfov_deg, d_max;
+    int32_t parent;  // body index or -1
+    int32_t pad;
+};
+
+// Per-body constants: tree root and local-frame bounding sphere.
+struct alignas(16) BodyInfo {
+    float cx, cy, cz, r;
+    int32_t root;
+    int32_t pad[3];
+};
+
+// Per-(env,cam) view record written by the prologue (128 B).
+struct alignas(16) ViewRec {
+    float r[9];            // camera->world rotation, row-major
+    float o[3];            // camera origin (world)
+    float ax, bx, ay, by;  // u = x*ax + bx, v = y*ay + by (intrinsics mode)
+    float dmax;            // float32(d_max)
+    int32_t nlinks;        // links surviving the view cull
+    int32_t read_slot;     // latency ring slot to read for this env (-1: current frame)
+    int32_t pad0;
+    unsigned long long hu; // rng prefix absorb(..step, env, cam) of the uniform stream
+    unsigned long long hn; // same for the normal stream
+    float pad1[8];
+};
+static_assert(sizeof(ViewRec) == 128, "ViewRec must be 128 B");
+
+// Per-(env,cam,link) record: camera-frame -> link-frame ray transform + pixel rect (64 B).
+struct alignas(16) LinkRec {
+    float m[9];            // d_link = M * d_cam
+    float o[3];            // camera origin in link frame
+    int32_t root;          // link tree root
+    int16_t x0, x1, y0, y1;
+};
+static_assert(sizeof(LinkRec) == 64, "LinkRec must be 64 B");
+
+// ---------------------------------------------------------------------------
+// counter-based RNG (rng.py:30-99)
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kGolden = 0x9E3779B97F4A7C15ULL;
+constexpr unsigned long long kMixA = 0xBF58476D1CE4E5B9ULL;
+constexpr unsigned long long kMixB = 0x94D049BB133111EBULL;
+constexpr unsigned long long kDomU1 = 0x9A4C93AED1F3B217ULL;
+constexpr unsigned long long kDomU2 = 0x6E2F1D84C5A7093BULL;
+
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 30;
+    x *= kMixA;
+    x ^= x >> 27;
+    x *= kMixB;
+    x ^= x >> 31;
+    return x;
+}
+
+__host__ __device__ __forceinline__ unsigned long long absorb(unsigned long long h, unsigned long long v) {
+    return mix64(h ^ mix64(v + kGolden));
+}
+
+// uniform in [0,1) from the top 53 bits (rng.py:78-80)
+__device__ __forceinline__ double unit53(unsigned long long h) {
+    return static_cast<double>(h >> 11) * 0x1p-53;
+}
+
+// standard normal by Box-Muller on two domain-separated sub-hashes (rng.py:94-99)
+__device__ __forceinline__ double normal_from_hash(unsigned long long h) {
+    const double u1 = static_cast<double>((absorb(h, kDomU1) >> 11) + 1ULL) * 0x1p-53;
+    const double u2 = static_cast<double>(absorb(h, kDomU2) >> 11) * 0x1p-53;
+    // __dmul_rn: keep numpy's unfused rounding
+    return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+}
+
+// apply_noise_dropout for one pixel (sensor.py:77-82). ru/rn: row prefixes
+// absorb(.., row); x: column counter.
+__device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru, unsigned long long rn,
+                                              unsigned long long x, double noise_scale, double dropout_p,
+                                              double fill, double dmax) {
+    const bool drop = unit53(absorb(ru, x)) < dropout_p;
+    const double g = normal_from_hash(absorb(rn, x));
+    double v = __dmul_rn(static_cast<double>(depth), __dadd_rn(1.0, __dmul_rn(noise_scale, g)));
+    v = drop ? fill : v;
+    v = v > 1e-6 ? v : 1e-6;       // np.clip lower (DEPTH_FLOOR, sensor.py:35)
+    v = v < dmax ? v : dmax;       // np.clip upper
+    return static_cast<float>(v);
+}
+
+// ---------------------------------------------------------------------------
+// closest-hit traversal (numba_backend.py:124-152 semantics, fp32, ordered)
+// ---------------------------------------------------------------------------
+struct TraceCounters {
+    unsigned int nodes = 0;
+    unsigned int tris = 0;
+};
+
+// Returns the nearest hit parameter t in (1e-6, tmax] or +inf when nothing
+// is hit (the caller then keeps its bound; numba_backend.py:206-208).
+// `stack` points at this thread's column of a [kStack][kBlock] shared array.
+template <bool COUNT>
+__device__ __forceinline__ float trace(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                       int32_t root, float ox, float oy, float oz, float dx, float dy,
+                                       float dz, float tmax, int* __restrict__ stack, TraceCounters& ctr) {
+    // zero direction components: a huge reciprocal turns the slab into a
+    // containment test like _slab_hit's d == 0 branch (numba_backend.py:76-78)
+    const float tiny = 1e-30f;
+    const float idx = 1.0f / (fabsf(dx) > tiny ? dx : copysignf(tiny, dx));
+    const float idy = 1.0f / (fabsf(dy) > tiny ? dy : copysignf(tiny, dy));
+    const float idz = 1.0f / (fabsf(dz) > tiny ? dz : copysignf(tiny, dz));
+    const float oxd = ox * idx, oyd = oy * idy, ozd = oz * idz;
+
+    float best = tmax;
+    bool hit = false;
+    int sp = 0;
+    int32_t ref = root;
+    while (true) {
+        while (ref >= 0) {
+            const float4* n = nodes + 4 * static_cast<int64_t>(ref);
+            const float4 bx = __ldg(n + 0);  // c0 x lo/hi, c0 y lo/hi
+            const float4 by = __ldg(n + 1);  // c1 x lo/hi, c1 y lo/hi
+            const float4 bz = __ldg(n + 2);  // c0 z lo/hi, c1 z lo/hi
+            const int4 rf = __ldg(reinterpret_cast<const int4*>(n + 3));
+            if (COUNT) ++ctr.nodes;
+            const float a0 = fmaf(bx.x, idx, -oxd), a1 = fmaf(bx.y, idx, -oxd);
+            const float a2 = fmaf(bx.z, idy, -oyd), a3 = fmaf(bx.w, idy, -oyd);
+            const float a4 = fmaf(bz.x, idz, -ozd), a5 = fmaf(bz.y, idz, -ozd);
+            const float c0min = fmaxf(fmaxf(fminf(a0, a1), fminf(a2, a3)), fmaxf(fminf(a4, a5), 0.0f));
+            const float c0max = fminf(fminf(fmaxf(a0, a1), fmaxf(a2, a3)), fminf(fmaxf(a4, a5), best));
+            const float b0 = fmaf(by.x, idx, -oxd), b1 = fmaf(by.y, idx, -oxd);
+            const float b2 = fmaf(by.z, idy, -oyd), b3 = fmaf(by.w, idy, -oyd);
+            const float b4 = fmaf(bz.z, idz, -ozd), b5 = fmaf(bz.w, idz, -ozd);
+            const float c1min = fmaxf(fmaxf(fminf(b0, b1), fminf(b2, b3)), fmaxf(fminf(b4, b5), 0.0f));
+            const float c1max = fminf(fminf(fmaxf(b0, b1), fmaxf(b2, b3)), fminf(fmaxf(b4, b5), best));
+            const bool h0 = c0min <= c0max;
+            const bool h1 = c1min <= c1max;
+            if (h0 && h1) {
+                int32_t near = rf.x, far = rf.y;
+                if (c1min < c0min) { near = rf.y; far = rf.x; }
+                stack[sp * kBlock] = far;
+                ++sp;
+                ref = near;
+            } else if (h0) {
+                ref = rf.x;
+            } else if (h1) {
+                ref = rf.y;
+            } else {
+                ref = sp > 0 ? stack[(--sp) * kBlock] : kExit;
+            }
+        }
+        if (ref == kExit) break;
+        // leaf: ~((first << 3) | (count - 1))
+        const int32_t v = ~ref;
+        const int32_t first = v >> 3;
+        const int32_t cnt = (v & 7) + 1;
+        for (int32_t i = 0; i < cnt; ++i) {
+            const float4* t = tris + 3 * static_cast<int64_t>(first + i);
+            const float4 v0 = __ldg(t + 0);
+            const float4 e1 = __ldg(t + 1);
+            const float4 e2 = __ldg(t + 2);
+            if (COUNT) ++ctr.tris;
+            // Moller-Trumbore, double-sided (numba_backend.py:37-69)
+            const float px = dy * e2.z - dz * e2.y;
+            const float py = dz * e2.x - dx * e2.z;
+            const float pz = dx * e2.y - dy * e2.x;
+            const float det = e1.x * px + e1.y * py + e1.z * pz;
+            const float inv = 1.0f / det;
+            const float tx = ox - v0.x, ty = oy - v0.y, tz = oz - v0.z;
+            const float u = (tx * px + ty * py + tz * pz) * inv;
+            const float qx = ty * e1.z - tz * e1.y;
+            const float qy = tz * e1.x - tx * e1.z;
+            const float qz = tx * e1.y - ty * e1.x;
+            const float w = (dx * qx + dy * qy + dz * qz) * inv;
+            const float tt = (e2.x * qx + e2.y * qy + e2.z * qz) * inv;
+            const bool ok = fabsf(det) >= 1e-12f && u >= -kBaryEps && u <= 1.0f + kBaryEps && w >= -kBaryEps &&
+                            u + w <= 1.0f + kBaryEps && tt > kRayEps && tt <= best;
+            if (ok) {
+                best = tt;
+                hit = true;
+            }
+        }
+        ref = sp > 0 ? stack[(--sp) * kBlock] : kExit;
+        if (ref == kExit) break;
+    }
+    return hit ? best : __int_as_float(0x7f800000);
+}
+
+}  // namespace mdrt

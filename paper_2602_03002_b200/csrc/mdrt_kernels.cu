@@ -1,0 +1,434 @@
+// CUDA kernels of the B200 multi-depth renderer (sm_100a).
+//
+//   prologue_kernel  (K4)  per-(env,cam) camera pose + intrinsics + link cull list.
+//                          Replaces Scene.camera_world_poses (scene.py:279-295),
+//                          ray_grids (scene.py:304-329) and the per-ray body
+//                          transform of numba_backend.py:193-202.
+//   render_kernel (K1+K2+K3) one warp per 8x4 pixel tile: link traversal in link
+//                          frames, terrain traversal, fused sensor epilogue and
+//                          latency ring. Replaces _render_kernel
+//                          (numba_backend.py:155-219), apply_noise_dropout
+//                          (sensor.py:55-82) and FrameBuffer (sensor.py:103-150).
+//   noise_kernel, gather_kernel, select_kernel, downsample_kernel: standalone
+//                          sensor-stage operators (sensor.py:55-150).
+#include "mdrt_kernels.h"
+
+#include <cmath>
+
+namespace mdrt {
+
+// ---------------------------------------------------------------------------
+// f64 pose helpers (transforms.py:32-58, 151-156). __d*_rn keeps numpy rounding.
+// ---------------------------------------------------------------------------
+struct Q { double w, x, y, z; };
+struct V3 { double x, y, z; };
+
+__device__ __forceinline__ Q qnorm(Q q) {
+    const double n = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q.w, q.w), __dmul_rn(q.x, q.x)),
+                                              __dmul_rn(q.y, q.y)), __dmul_rn(q.z, q.z)));
+    return {q.w / n, q.x / n, q.y / n, q.z / n};
+}
+
+__device__ __forceinline__ Q qmul(Q a, Q b) {
+    Q r;
+    r.w = a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z;
+    r.x = a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y;
+    r.y = a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x;
+    r.z = a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w;
+    return qnorm(r);
+}
+
+__device__ __forceinline__ V3 qrot(Q q, V3 v) {
+    // v + w t + q_v x t,  t = 2 q_v x v
+    const double tx = 2.0 * (q.y * v.z - q.z * v.y);
+    const double ty = 2.0 * (q.z * v.x - q.x * v.z);
+    const double tz = 2.0 * (q.x * v.y - q.y * v.x);
+    return {v.x + q.w * tx + (q.y * tz - q.z * ty), v.y + q.w * ty + (q.z * tx - q.x * tz),
+            v.z + q.w * tz + (q.x * ty - q.y * tx)};
+}
+
+__device__ __forceinline__ void qmat(Q q, double m[9]) {
+    const double w = q.w, x = q.x, y = q.y, z = q.z;
+    m[0] = 1 - 2 * (y * y + z * z); m[1] = 2 * (x * y - w * z);     m[2] = 2 * (x * z + w * y);
+    m[3] = 2 * (x * y + w * z);     m[4] = 1 - 2 * (x * x + z * z); m[5] = 2 * (y * z - w * x);
+    m[6] = 2 * (x * z - w * y);     m[7] = 2 * (y * z + w * x);     m[8] = 1 - 2 * (x * x + y * y);
+}
+
+// Conservative range of slopes s = a/Z of rays through the origin that touch a
+// circle of radius r centred at (A, Z) (projection of the link sphere).
+__device__ __forceinline__ bool slope_range(double A, double Z, double r, double& lo, double& hi) {
+    const double den = Z * Z - r * r;
+    const double disc = A * A + Z * Z - r * r;
+    if (!(den > 0.0) || !(disc > 0.0)) return false;  // unbounded -> caller uses full range
+    const double s = sqrt(disc);
+    lo = (A * Z - r * s) / den;
+    hi = (A * Z + r * s) / den;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// K4 prologue: one warp per (env, cam); lanes walk the links.
+// ---------------------------------------------------------------------------
+static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t view = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (view >= static_cast<int64_t>(p.N) * p.C) return;
+    const int e = static_cast<int>(view / p.C);
+    const int c = static_cast<int>(view - static_cast<int64_t>(e) * p.C);
+    const CamRig rig = p.rigs[c];
+
+    // ---- camera world pose (scene.py:279-295) ----
+    V3 t;
+    Q q;
+    if (p.cam_pos) {
+        const float* cp = p.cam_pos + view * 3;
+        const float* cq = p.cam_rot + view * 4;
+        t = {cp[0], cp[1], cp[2]};
+        q = {cq[0], cq[1], cq[2], cq[3]};
+    } else {
+        t = {rig.mount_pos[0], rig.mount_pos[1], rig.mount_pos[2]};
+        q = {rig.mount_rot[0], rig.mount_rot[1], rig.mount_rot[2], rig.mount_rot[3]};
+        if (rig.parent >= 0) {
+            const int64_t bi = static_cast<int64_t>(e) * p.B + rig.parent;
+            const float* bp = p.body_pos + bi * 3;
+            const float* bq = p.body_rot + bi * 4;
+            Q pq = qnorm(qnorm({bq[0], bq[1], bq[2], bq[3]}));
+            V3 rt = qrot(pq, t);
+            t = {bp[0] + rt.x, bp[1] + rt.y, bp[2] + rt.z};
+            q = qnorm(qmul(pq, q));
+        }
+        if (p.off_pos) {
+            const float* op = p.off_pos + view * 3;
+            const float* oq = p.off_rot + view * 4;
+            Q offq = qnorm(qnorm({oq[0], oq[1], oq[2], oq[3]}));
+            V3 rt = qrot(q, {op[0], op[1], op[2]});
+            t = {t.x + rt.x, t.y + rt.y, t.z + rt.z};
+            q = qnorm(qmul(q, offq));
+        }
+    }
+    double R[9];
+    qmat(q, R);
+
+    // ---- intrinsics (camera.py:51-65, with_fov_delta camera.py:92-95) ----
+    const double delta = p.fov_delta ? static_cast<double>(p.fov_delta[view]) : 0.0;
+    const double kDeg = 3.141592653589793 / 180.0;
+    const double fx = (p.W / 2.0) / tan(((rig.hfov_deg + delta) * kDeg) / 2.0);
+    const double fy = (p.H / 2.0) / tan(((rig.vfov_deg + delta) * kDeg) / 2.0);
+    const double cx = p.W / 2.0, cy = p.H / 2.0;
+    const bool grid = p.grid_mode;
+
+    // ---- link cull list ----
+    int count = 0;
+    for (int base = 0; base < p.B; base += 32) {
+        const int b = base + lane;
+        bool keep = false;
+        LinkRec rec;
+        if (b < p.B) {
+            const BodyInfo bi = p.bodies[b];
+            const int64_t k = static_cast<int64_t>(e) * p.B + b;
+            const float* bp = p.body_pos + k * 3;
+            const float* bq = p.body_rot + k * 4;
+            const Q lq = qnorm({bq[0], bq[1], bq[2], bq[3]});
+            double L[9];
+            qmat(lq, L);  // link -> world
+            // sphere centre in world, then camera frame
+            const double cwx = bp[0] + L[0] * bi.cx + L[1] * bi.cy + L[2] * bi.cz;
+            const double cwy = bp[1] + L[3] * bi.cx + L[4] * bi.cy + L[5] * bi.cz;
+            const double cwz = bp[2] + L[6] * bi.cx + L[7] * bi.cy + L[8] * bi.cz;
+            const double wx = cwx - t.x, wy = cwy - t.y, wz = cwz - t.z;
+            const double X = R[0] * wx + R[3] * wy + R[6] * wz;
+            const double Y = R[1] * wx + R[4] * wy + R[7] * wz;
+            const double Z = R[2] * wx + R[5] * wy + R[8] * wz;
+            const double r = bi.r;
+            const double dist = sqrt(X * X + Y * Y + Z * Z);
+            keep = (dist - r) <= rig.d_max * (1.0 + 1e-6) + 1e-6;
+            int x0 = 0, x1 = p.W - 1, y0 = 0, y1 = p.H - 1;
+            if (keep && !grid && !p.no_cull) {
+                keep = Z + r > 0.0;  // every ray point with t > 0 has camera z = t > 0
+                double lo, hi;
+                if (keep && Z - r > 1e-9 && slope_range(X, Z, r, lo, hi)) {
+                    x0 = max(x0, static_cast<int>(floor(lo * fx + cx - 0.5)) - 1);
+                    x1 = min(x1, static_cast<int>(ceil(hi * fx + cx - 0.5)) + 1);
+                }
+                if (keep && Z - r > 1e-9 && slope_range(Y, Z, r, lo, hi)) {
+                    y0 = max(y0, static_cast<int>(floor(lo * fy + cy - 0.5)) - 1);
+                    y1 = min(y1, static_cast<int>(ceil(hi * fy + cy - 0.5)) + 1);
+                }
+                keep = keep && x0 <= x1 && y0 <= y1;
+            }
+            if (keep) {
+                // M = L^T R (camera frame -> link frame), o = L^T (t - p)
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j)
+                        rec.m[i * 3 + j] = static_cast<float>(L[0 * 3 + i] * R[0 * 3 + j] +
+                                                              L[1 * 3 + i] * R[1 * 3 + j] +
+                                                              L[2 * 3 + i] * R[2 * 3 + j]);
+                const double ox = t.x - bp[0], oy = t.y - bp[1], oz = t.z - bp[2];
+                rec.o[0] = static_cast<float>(L[0] * ox + L[3] * oy + L[6] * oz);
+                rec.o[1] = static_cast<float>(L[1] * ox + L[4] * oy + L[7] * oz);
+                rec.o[2] = static_cast<float>(L[2] * ox + L[5] * oy + L[8] * oz);
+                rec.root = bi.root;
+                rec.x0 = static_cast<int16_t>(x0);
+                rec.x1 = static_cast<int16_t>(x1);
+                rec.y0 = static_cast<int16_t>(y0);
+                rec.y1 = static_cast<int16_t>(y1);
+            }
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int slot = count + __popc(mask & ((1u << lane) - 1u));
+            p.links[view * p.B + slot] = rec;
+        }
+        count += __popc(mask);
+    }
+
+    // ---- view record ----
+    if (lane == 0) {
+        ViewRec v;
+        for (int i = 0; i < 9; ++i) v.r[i] = static_cast<float>(R[i]);
+        v.o[0] = static_cast<float>(t.x);
+        v.o[1] = static_cast<float>(t.y);
+        v.o[2] = static_cast<float>(t.z);
+        v.ax = static_cast<float>(1.0 / fx);
+        v.bx = static_cast<float>((0.5 - cx) / fx);
+        v.ay = static_cast<float>(1.0 / fy);
+        v.by = static_cast<float>((0.5 - cy) / fy);
+        v.dmax = static_cast<float>(rig.d_max);
+        v.nlinks = count;
+        v.read_slot = -1;
+        v.pad0 = 0;
+        const unsigned long long genv = static_cast<unsigned long long>(p.env_offset + e);
+        v.hu = absorb(absorb(p.hu_step, genv), static_cast<unsigned long long>(c));
+        v.hn = absorb(absorb(p.hn_step, genv), static_cast<unsigned long long>(c));
+        if (p.latency) {
+            // bisect_right(times, now - delay) - 1, clamped at 0 (sensor.py:138-139)
+            const double target = p.now - p.delays[e];
+            int lo = 0, hi = p.ring_count;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (target < p.ring_times[mid]) hi = mid;
+                else lo = mid + 1;
+            }
+            const int kk = lo - 1 < 0 ? 0 : lo - 1;
+            const int slot = p.ring_order[kk];
+            v.read_slot = slot == p.write_slot ? -1 : slot;
+            if (c == 0 && p.read_slot_out) p.read_slot_out[e] = slot;
+        }
+        for (int i = 0; i < 8; ++i) v.pad1[i] = 0.f;
+        p.views[view] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1+K2+K3: render + fused sensor epilogue. One warp = one 8x4 tile of a view.
+// ---------------------------------------------------------------------------
+template <bool COUNT>
+static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p) {
+    __shared__ int s_stack[kStack * kBlock];
+    int* stack = s_stack + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) >> 5;
+    const int64_t total = static_cast<int64_t>(p.N) * p.C * p.tiles_per_view;
+    if (gw >= total) return;
+    const int64_t view = gw / p.tiles_per_view;
+    const int tile = static_cast<int>(gw - view * p.tiles_per_view);
+    const int ty = tile / p.tiles_x;
+    const int tx = tile - ty * p.tiles_x;
+    const int px = tx * kTileW + (lane & (kTileW - 1));
+    const int py = ty * kTileH + (lane >> 3);
+    const bool active = px < p.W && py < p.H;
+    const int e = static_cast<int>(view / p.C);
+    const int c = static_cast<int>(view - static_cast<int64_t>(e) * p.C);
+
+    const ViewRec& V = p.views[view];
+    const float4 in = *reinterpret_cast<const float4*>(&V.ax);     // ax bx ay by
+    const float dmax = V.dmax;
+    const int nlinks = V.nlinks;
+
+    // camera-frame direction and scale (camera.py:81-90)
+    float dcx, dcy, dcz, m;
+    if (p.ray_dirs) {
+        const int64_t er = p.ray_envs > 1 ? e : 0;
+        const int64_t pix = ((er * p.C + c) * p.H + (active ? py : 0)) * p.W + (active ? px : 0);
+        dcx = p.ray_dirs[pix * 3 + 0];
+        dcy = p.ray_dirs[pix * 3 + 1];
+        dcz = p.ray_dirs[pix * 3 + 2];
+        m = p.ray_scale[pix];
+    } else {
+        dcx = fmaf(static_cast<float>(px), in.x, in.y);
+        dcy = fmaf(static_cast<float>(py), in.z, in.w);
+        dcz = 1.0f;
+        m = sqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
+    }
+    const float inv_m = 1.0f / m;
+    TraceCounters ctr;
+    float z = dmax;
+
+    // ---- K2: links in their local frames (numba_backend.py:190-208) ----
+    for (int k = 0; k < nlinks; ++k) {
+        const LinkRec& L = p.links[view * p.B + k];
+        const int4 tail = *reinterpret_cast<const int4*>(&L.root);  // root | x0,x1 | y0,y1 | pad
+        const int x0 = static_cast<int16_t>(tail.y & 0xffff), x1 = tail.y >> 16;
+        const int y0 = static_cast<int16_t>(tail.z & 0xffff), y1 = tail.z >> 16;
+        const bool want = active && px >= x0 && px <= x1 && py >= y0 && py <= y1;
+        if (!__any_sync(0xffffffffu, want)) continue;
+        if (want) {
+            const float4 m0 = *reinterpret_cast<const float4*>(&L.m[0]);
+            const float4 m1 = *reinterpret_cast<const float4*>(&L.m[4]);
+            const float4 m2 = *reinterpret_cast<const float4*>(&L.m[8]);  // m8 o0 o1 o2
+            const float ldx = m0.x * dcx + m0.y * dcy + m0.z * dcz;
+            const float ldy = m0.w * dcx + m1.x * dcy + m1.y * dcz;
+            const float ldz = m1.z * dcx + m1.w * dcy + m2.x * dcz;
+            const float bound = p.early_termination ? z : dmax;
+            const float tt = trace<COUNT>(p.nodes, p.tris, tail.x, m2.y, m2.z, m2.w, ldx, ldy, ldz,
+                                          bound * inv_m, stack, ctr);
+            const float cand = m * tt;
+            if (cand < z) z = cand;
+        }
+    }
+
+    // ---- K1: terrain in the world frame (numba_backend.py:209-218) ----
+    if (p.terrain_root >= 0 && active) {
+        const float4 r0 = *reinterpret_cast<const float4*>(&V.r[0]);  // r0..r3
+        const float4 r1 = *reinterpret_cast<const float4*>(&V.r[4]);  // r4..r7
+        const float4 r2 = *reinterpret_cast<const float4*>(&V.r[8]);  // r8, o0, o1, o2
+        const float wdx = r0.x * dcx + r0.y * dcy + r0.z * dcz;
+        const float wdy = r0.w * dcx + r1.x * dcy + r1.y * dcz;
+        const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
+        const float bound = p.early_termination ? z : dmax;
+        const float tt = trace<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
+                                      bound * inv_m, stack, ctr);
+        const float cand = m * tt;
+        if (cand < z) z = cand;
+    }
+
+    if (COUNT) {
+        unsigned int nn = ctr.nodes, nt = ctr.tris;
+        for (int off = 16; off > 0; off >>= 1) {
+            nn += __shfl_xor_sync(0xffffffffu, nn, off);
+            nt += __shfl_xor_sync(0xffffffffu, nt, off);
+        }
+        if (lane == 0) {
+            atomicAdd(p.counters + 0, static_cast<unsigned long long>(nn));
+            atomicAdd(p.counters + 1, static_cast<unsigned long long>(nt));
+        }
+    }
+    if (!active) return;
+
+    // ---- K3: fused epilogue ----
+    const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
+    if (p.out_clean) p.out_clean[o] = z;
+    float val = z;
+    if (p.sensor) {
+        const unsigned long long ru = absorb(V.hu, static_cast<unsigned long long>(py));
+        const unsigned long long rn = absorb(V.hn, static_cast<unsigned long long>(py));
+        val = sensor_apply(z, ru, rn, static_cast<unsigned long long>(px), p.noise_scale, p.dropout_p,
+                           p.fill[c], p.dmax64[c]);
+    }
+    if (p.ring) {
+        const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
+        p.ring[static_cast<int64_t>(p.write_slot) * frame + o] = val;
+        const int rs = V.read_slot;
+        if (rs >= 0) val = p.ring[static_cast<int64_t>(rs) * frame + o];
+    }
+    p.out[o] = val;
+}
+
+
+// ---------------------------------------------------------------------------
+// standalone sensor-stage operators
+// ---------------------------------------------------------------------------
+static __global__ void noise_kernel(NoiseParams p) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
+    if (i >= total) return;
+    const int x = static_cast<int>(i % p.W);
+    const int64_t r = i / p.W;
+    const int y = static_cast<int>(r % p.H);
+    const int64_t r2 = r / p.H;
+    const int c = static_cast<int>(r2 % p.C);
+    const int64_t e = r2 / p.C;
+    const unsigned long long genv = static_cast<unsigned long long>(p.env_offset + e);
+    const unsigned long long ru =
+        absorb(absorb(absorb(p.hu_step, genv), static_cast<unsigned long long>(c)), static_cast<unsigned long long>(y));
+    const unsigned long long rn =
+        absorb(absorb(absorb(p.hn_step, genv), static_cast<unsigned long long>(c)), static_cast<unsigned long long>(y));
+    p.out[i] = sensor_apply(p.in[i], ru, rn, static_cast<unsigned long long>(x), p.noise_scale, p.dropout_p,
+                            p.fill[c], p.dmax[c]);
+}
+
+static __global__ void gather_kernel(GatherParams p) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.N * p.per_env) return;
+    const int64_t e = i / p.per_env;
+    const int s = p.slot[e];
+    p.out[i] = p.frames[s][i];
+}
+
+static __global__ void select_kernel(SelectParams p) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= p.N) return;
+    const double target = p.now - p.delays[e];
+    int lo = 0, hi = p.K;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (target < p.times[mid]) hi = mid;
+        else lo = mid + 1;
+    }
+    const int k = lo - 1 < 0 ? 0 : lo - 1;
+    p.slot[e] = p.order[k];
+}
+
+static __global__ void downsample_kernel(DownsampleParams p) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int ho = p.H / p.f, wo = p.W / p.f;
+    if (i >= p.planes * ho * wo) return;
+    const int bx = static_cast<int>(i % wo);
+    const int64_t r = i / wo;
+    const int by = static_cast<int>(r % ho);
+    const int64_t plane = r / ho;
+    const float* src = p.in + (plane * p.H + static_cast<int64_t>(by) * p.f) * p.W + static_cast<int64_t>(bx) * p.f;
+    float mn = src[0];
+    for (int dy = 0; dy < p.f; ++dy)
+        for (int dx = 0; dx < p.f; ++dx) {
+            const float v = src[static_cast<int64_t>(dy) * p.W + dx];
+            mn = v < mn ? v : mn;
+        }
+    p.out[i] = mn;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static unsigned grid_for(int64_t threads, int block) {
+    return static_cast<unsigned>((threads + block - 1) / block);
+}
+
+void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s) {
+    prologue_kernel<<<grid_for(views * 32, 128), 128, 0, s>>>(p);
+}
+
+void launch_render(const RenderParams& p, int64_t warps, bool count, cudaStream_t s) {
+    if (count)
+        render_kernel<true><<<grid_for(warps * 32, kBlock), kBlock, 0, s>>>(p);
+    else
+        render_kernel<false><<<grid_for(warps * 32, kBlock), kBlock, 0, s>>>(p);
+}
+
+void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s) {
+    noise_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);
+}
+
+void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s) {
+    gather_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);
+}
+
+void launch_select(const SelectParams& p, int64_t n, cudaStream_t s) {
+    select_kernel<<<grid_for(n, 256), 256, 0, s>>>(p);
+}
+
+void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s) {
+    downsample_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);
+}
+
+}  // namespace mdrt

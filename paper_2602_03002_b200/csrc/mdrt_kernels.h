@@ -1,0 +1,104 @@
+// Kernel parameter blocks and declarations (see mdrt_kernels.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "mdrt_device.cuh"
+
+namespace mdrt {
+
+struct PrologueParams {
+    int32_t N, C, B, W, H;
+    int64_t env_offset;
+    const CamRig* rigs;
+    const BodyInfo* bodies;
+    const float* body_pos;
+    const float* body_rot;
+    const float* off_pos;
+    const float* off_rot;
+    const float* fov_delta;
+    const float* cam_pos;   // seam mode
+    const float* cam_rot;
+    int32_t grid_mode;      // per-pixel ray grids given: no image-space cull
+    int32_t no_cull;
+    unsigned long long hu_step, hn_step;
+    // latency selection
+    int32_t latency;
+    int32_t ring_count;
+    int32_t write_slot;
+    double now;
+    const double* delays;
+    double ring_times[32];
+    int32_t ring_order[32];
+    int32_t* read_slot_out;
+    ViewRec* views;
+    LinkRec* links;
+};
+
+struct RenderParams {
+    int32_t N, C, B, W, H;
+    int32_t tiles_x, tiles_per_view;
+    int32_t early_termination;
+    int32_t terrain_root;
+    const float4* nodes;
+    const float4* tris;
+    const ViewRec* views;
+    const LinkRec* links;
+    const float* ray_dirs;
+    const float* ray_scale;
+    int32_t ray_envs;
+    int32_t sensor;
+    double noise_scale, dropout_p;
+    double fill[64];
+    double dmax64[64];
+    float* ring;
+    int32_t write_slot;
+    float* out_clean;
+    float* out;
+    unsigned long long* counters;
+};
+
+struct NoiseParams {
+    const float* in;
+    float* out;
+    int32_t N, C, H, W;
+    int64_t env_offset;
+    unsigned long long hu_step, hn_step;
+    double noise_scale, dropout_p;
+    double fill[64];
+    double dmax[64];
+};
+
+struct GatherParams {
+    const float* frames[32];
+    const int32_t* slot;
+    float* out;
+    int64_t N, per_env;
+};
+
+struct SelectParams {
+    double times[32];
+    int32_t order[32];
+    int32_t K;
+    double now;
+    const double* delays;
+    int32_t* slot;
+    int64_t N;
+};
+
+struct DownsampleParams {
+    const float* in;
+    float* out;
+    int64_t planes;
+    int32_t H, W, f;
+};
+
+// Host-side launchers (defined next to the kernels so templates instantiate there).
+void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s);
+void launch_render(const RenderParams& p, int64_t warps, bool count, cudaStream_t s);
+void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s);
+void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s);
+void launch_select(const SelectParams& p, int64_t n, cudaStream_t s);
+void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s);
+
+}  // namespace mdrt

@@ -1,0 +1,97 @@
+"""``render_batch`` for the reference's backend seam, executed by libmdrt.so.
+
+Drop-in for ``multidepth.kernels.numba_backend.render_batch``
+(/root/reference/pkg/src/multidepth/kernels/numba_backend.py:222-234): same
+arguments, same in-place write of ``out`` (N,C,H,W) float32. Inputs may be
+host numpy arrays (as the reference passes them) or CUDA tensors.
+
+The reference hands over its median-split BVH forest (FlatGeometry,
+scene.py:49-147); the GPU path rebuilds its own SAH BVHs from the triangle
+arrays once per FlatGeometry object (cached; geometry is immutable,
+scene.py:150-157) and then only per-call poses, camera poses and ray grids
+cross the boundary.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from .. import _native
+from ..scene import _cuda_device
+
+_cache: dict = {}
+_lock = threading.Lock()
+_MAX_CACHE = 4
+
+
+def _tri_mesh(v0, v1, v2):
+    tris = np.stack([np.asarray(v0, np.float64), np.asarray(v1, np.float64),
+                     np.asarray(v2, np.float64)], axis=1)          # (F,3,3)
+    f = len(tris)
+    return tris.reshape(-1, 3), np.arange(3 * f, dtype=np.int64).reshape(f, 3)
+
+
+def _context(flat, C, H, W, d_max, device):
+    key = (id(flat), C, H, W, tuple(float(x) for x in d_max), device.index)
+    with _lock:
+        hit = _cache.get(key)
+        if hit is not None and hit[0] is flat:
+            return hit[1]
+        ctx = _native.Context(device.index)
+        offs = np.asarray(flat.body_tri_offsets, dtype=np.int64)
+        for b in range(len(flat.body_root)):
+            s, e = int(offs[b]), int(offs[b + 1])
+            ctx.add_body(*_tri_mesh(flat.tri_v0[s:e], flat.tri_v1[s:e], flat.tri_v2[s:e]))
+        if len(flat.g_tri_v0):
+            ctx.set_terrain(*_tri_mesh(flat.g_tri_v0, flat.g_tri_v1, flat.g_tri_v2))
+        # seam mode: camera poses and ray grids arrive per call; the rig only carries d_max
+        ctx.set_cameras(W, H, [90.0] * C, [90.0] * C, list(d_max), [-1] * C, np.zeros((C, 3)),
+                        np.tile([1.0, 0.0, 0.0, 0.0], (C, 1)))
+        ctx.commit()
+        if len(_cache) >= _MAX_CACHE:
+            _cache.pop(next(iter(_cache)))
+        _cache[key] = (flat, ctx)
+        return ctx
+
+
+def _dev(x, device):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(device, non_blocking=True)
+
+
+def render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,
+                 early_termination, out, threads=None):
+    n, c, h, w = out.shape
+    device = out.device if isinstance(out, torch.Tensor) and out.is_cuda else _cuda_device(None)
+    d_max = np.broadcast_to(np.asarray(d_max, np.float64), (c,))
+    ctx = _context(flat, c, h, w, d_max, device)
+    b = len(flat.body_root)
+    bp, bq = _dev(body_pos, device), _dev(body_rot, device)
+    cp, cq = _dev(cam_pos, device), _dev(cam_rot, device)
+    rd, rs = _dev(ray_dirs, device), _dev(ray_scale, device)
+    if tuple(rd.shape[1:]) != (c, h, w, 3) or tuple(rs.shape[1:]) != (c, h, w):
+        raise ValueError("ray grids must be shaped (RN,C,H,W,3) / (RN,C,H,W)")
+    dev_out = out if isinstance(out, torch.Tensor) and out.is_cuda and out.is_contiguous() else \
+        torch.empty((n, c, h, w), dtype=torch.float32, device=device)
+    a = _native.StepArgs()
+    a.num_envs = n
+    a.flags = _native.EARLY_TERMINATION if early_termination else 0
+    a.body_pos = bp.data_ptr() if b else None
+    a.body_rot = bq.data_ptr() if b else None
+    a.cam_pos = cp.data_ptr()
+    a.cam_rot = cq.data_ptr()
+    a.ray_dirs = rd.data_ptr()
+    a.ray_scale = rs.data_ptr()
+    a.ray_envs = int(rd.shape[0])
+    a.out = dev_out.data_ptr()
+    ctx.render(a, torch.cuda.current_stream(device).cuda_stream)
+    if dev_out is not out:
+        if isinstance(out, torch.Tensor):
+            out.copy_(dev_out)
+        else:
+            out[...] = dev_out.cpu().numpy()
+    return out

@@ -1,0 +1,83 @@
+"""The fused per-step depth pipeline: render + sensor + latency in one kernel.
+
+Semantically identical to the reference sequence
+
+    frame = render(scene, timestamp=t)                                   # scene.py:332-348
+    noisy = apply_noise_dropout(frame.data, cfg, d_max=..., step=step)   # sensor.py:55-82
+    buf.push(DepthFrame(noisy, t))                                       # sensor.py:122-131
+    obs = buf.fetch_delayed_batch(t, delays)                             # sensor.py:141-150
+
+but executed as two launches (prologue + traversal) with the noise/dropout
+epilogue and the latency-ring write/read fused into the traversal kernel's
+tail, so each pixel's range is written to HBM once (ring) and the delayed
+observation once (obs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .scene import Scene
+from .sensor import FrameBuffer, SensorConfig, _delays_tensor
+
+
+def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: int = 0,
+                    frame_buffer: FrameBuffer | None = None, timestamp: float | None = None,
+                    delays=None, early_termination: bool = True, out: torch.Tensor | None = None,
+                    clean_out: torch.Tensor | None = None,
+                    counters: torch.Tensor | None = None) -> torch.Tensor:
+    """One simulation step of the multi-depth pipeline; returns the observation (N,C,H,W).
+
+    * ``sensor``: apply noise/dropout/clamp with counters (step, global env, cam, row, col).
+    * ``frame_buffer`` + ``timestamp`` + ``delays`` (N,): push the noisy frame
+      and return, per env, the newest frame with ts <= timestamp - delay.
+    * ``clean_out``: optionally also store the noise-free range image.
+    """
+    data = scene._new_frame(out)
+    a = scene._step_args(data, early_termination)
+    if clean_out is not None:
+        scene._new_frame(clean_out)
+        a.out_clean = clean_out.data_ptr()
+    keep = []
+    if sensor is not None:
+        a.flags |= _native.SENSOR
+        a.noise_scale = float(sensor.noise_scale)
+        a.dropout_p = float(sensor.dropout_p)
+        a.sensor_key = sensor.key
+        a.step = int(step)
+        if sensor.dropout_fill is not None:
+            fill = np.full(scene.num_cameras, float(sensor.dropout_fill), dtype=np.float64)
+            keep.append(fill)
+            a.fill = _native.dptr(fill)
+    if frame_buffer is not None:
+        if timestamp is None or delays is None:
+            raise ValueError("frame_buffer needs timestamp and delays")
+        d = _delays_tensor(delays, scene.device)
+        if tuple(d.shape) != (scene.num_envs,):
+            raise ValueError(f"delays must have shape ({scene.num_envs},)")
+        frame_buffer._ensure(scene.frame_shape, scene.device)
+        slot = frame_buffer._reserve(float(timestamp))
+        times = np.ascontiguousarray(frame_buffer._times, dtype=np.float64)
+        order = np.ascontiguousarray(frame_buffer._slots, dtype=np.int32)
+        keep += [times, order, d]
+        if frame_buffer._slot_buf is None or frame_buffer._slot_buf.shape[0] != scene.num_envs:
+            frame_buffer._slot_buf = torch.empty(scene.num_envs, dtype=torch.int32, device=scene.device)
+        a.flags |= _native.LATENCY
+        a.ring = frame_buffer._ring.data_ptr()
+        a.ring_slots = frame_buffer.capacity
+        a.write_slot = slot
+        a.ring_count = len(times)
+        a.ring_times = _native.dptr(times)
+        a.ring_order = order.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        a.now = float(timestamp)
+        a.delays = d.data_ptr()
+        a.read_slot = frame_buffer._slot_buf.data_ptr()
+    if counters is not None:
+        a.flags |= _native.COUNT
+        a.counters = counters.data_ptr()
+    scene._launch(a)
+    return data

@@ -1,0 +1,306 @@
+"""Batched multi-environment scenes rendered on a B200.
+
+Mirror of the reference ``multidepth.scene`` (/root/reference/pkg/src/multidepth/scene.py)
+with the state moved to the GPU:
+
+* geometry (body meshes in link frames + world terrain) is registered once;
+  the native library builds one SAH BVH per mesh and uploads it
+  (``mdrt_add_body``/``mdrt_set_terrain``/``mdrt_commit``) -- never rebuilt;
+* per-env body poses and camera randomisation live in CUDA tensors;
+* ``render`` launches the prologue (camera poses, intrinsics, link culling)
+  and the traversal kernel on the current torch stream and returns a CUDA
+  tensor ``[N, C, H, W]`` float32 of Euclidean range (misses read exactly
+  ``float32(d_max)``).
+
+There is no CPU path: constructing a Scene without a CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .camera import CameraModel
+from .mesh import TriMesh
+from .transforms import RigidPose, quat_identity
+
+
+@dataclass(frozen=True)
+class Body:
+    name: str
+    mesh: TriMesh
+    body_id: int = -1   # index in the native context (its BVH is built once)
+
+
+@dataclass
+class DepthFrame:
+    """Range depth [env, camera, row, col] in metres (scene.py:33-46)."""
+
+    data: object          # torch.Tensor (CUDA) or np.ndarray
+    timestamp: float = 0.0
+
+    def __post_init__(self):
+        if len(self.data.shape) != 4:
+            raise ValueError(f"depth data must be 4-D (N,C,H,W), got {tuple(self.data.shape)}")
+
+    @property
+    def shape(self) -> tuple[int, int, int, int]:
+        return tuple(self.data.shape)
+
+
+def _cuda_device(device) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("a CUDA device is required: the B200 renderer has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def _as_device_f32(x, device, shape=None) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=torch.float32)
+    else:
+        t = torch.as_tensor(np.asarray(x, dtype=np.float64), dtype=torch.float32).to(device)
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+class Scene:
+    """Shared immutable geometry + per-environment poses (scene.py:150-330).
+
+    ``env_offset`` is the global index of environment 0 of this scene; it keys
+    the sensor RNG so an env-sliced multi-GPU run reproduces the single-GPU
+    stream bit-for-bit.
+    """
+
+    def __init__(self, num_envs: int, bodies=(), cameras=(), terrain: TriMesh | None = None, *,
+                 device=None, env_offset: int = 0):
+        if num_envs < 1:
+            raise ValueError("num_envs must be >= 1")
+        self.num_envs = int(num_envs)
+        self.env_offset = int(env_offset)
+        entries = []
+        for i, entry in enumerate(bodies):
+            if isinstance(entry, Body):
+                name, mesh = entry.name, entry.mesh
+            elif isinstance(entry, tuple):
+                name, mesh = entry
+            else:
+                name, mesh = f"body{i}", entry
+            if mesh.num_faces == 0:
+                raise ValueError(f"body {name!r} has no triangles")
+            entries.append((str(name), mesh))
+        cams = tuple(cameras)
+        if not cams:
+            raise ValueError("scene needs at least one camera")
+        h, w = cams[0].height, cams[0].width
+        for cam in cams:
+            if (cam.height, cam.width) != (h, w):
+                raise ValueError("all cameras in a scene must share one resolution")
+            if cam.parent_body is not None and not 0 <= cam.parent_body < len(entries):
+                raise ValueError(f"camera {cam.name!r} parent_body {cam.parent_body} out of range")
+        if len(cams) > 64:
+            raise ValueError("at most 64 cameras per scene")
+        if terrain is not None and terrain.num_faces == 0:
+            raise ValueError("terrain mesh has no triangles")
+
+        self.device = _cuda_device(device)
+        self._ctx = _native.Context(self.device.index)
+        body_list = []
+        for name, mesh in entries:
+            body_list.append(Body(name, mesh, self._ctx.add_body(mesh.vertices, mesh.faces)))
+        self.bodies: tuple[Body, ...] = tuple(body_list)
+        self.terrain = terrain
+        if terrain is not None:
+            self._ctx.set_terrain(terrain.vertices, terrain.faces)
+        self.cameras: tuple[CameraModel, ...] = cams
+        self.height, self.width = h, w
+        self._ctx.set_cameras(
+            w, h, [c.hfov_deg for c in cams], [c.vfov_deg for c in cams], [c.d_max for c in cams],
+            [-1 if c.parent_body is None else c.parent_body for c in cams],
+            np.stack([c.mount.translation for c in cams]), np.stack([c.mount.rotation for c in cams]))
+        self._ctx.commit()
+        self.geometry_stats = self._ctx.stats()
+
+        n, b = self.num_envs, len(self.bodies)
+        self.body_positions = torch.zeros((n, b, 3), dtype=torch.float32, device=self.device)
+        self.body_rotations = torch.zeros((n, b, 4), dtype=torch.float32, device=self.device)
+        self.body_rotations[..., 0] = 1.0
+        self._rand_pos: torch.Tensor | None = None
+        self._rand_rot: torch.Tensor | None = None
+        self._rand_fov: torch.Tensor | None = None
+        self.d_max_per_camera = np.array([c.d_max for c in cams], dtype=np.float64)
+
+    # -- sizes -------------------------------------------------------------
+    @property
+    def num_bodies(self) -> int:
+        return len(self.bodies)
+
+    @property
+    def num_cameras(self) -> int:
+        return len(self.cameras)
+
+    @property
+    def frame_shape(self) -> tuple[int, int, int, int]:
+        return (self.num_envs, self.num_cameras, self.height, self.width)
+
+    # -- pose state (scene.py:227-253) --------------------------------------
+    def set_body_pose(self, env: int, body: int, pose: RigidPose) -> None:
+        if not 0 <= env < self.num_envs:
+            raise ValueError(f"env {env} out of range [0, {self.num_envs})")
+        if not 0 <= body < self.num_bodies:
+            raise ValueError(f"body {body} out of range [0, {self.num_bodies})")
+        self.body_positions[env, body] = torch.as_tensor(pose.translation, dtype=torch.float32)
+        self.body_rotations[env, body] = torch.as_tensor(pose.rotation, dtype=torch.float32)
+
+    def set_body_poses(self, positions, rotations, *, validate: bool = True) -> None:
+        """positions (N,B,3), rotations (N,B,4) wxyz; numpy or torch (any device).
+
+        Quaternions are normalised on the device (in f64) by the prologue
+        kernel, so any nonzero norm is accepted as in the reference.
+        ``validate=False`` skips the finite/zero-norm checks, which need a
+        device->host read for CUDA inputs.
+        """
+        n, b = self.num_envs, self.num_bodies
+        pos = _as_device_f32(positions, self.device)
+        rot = _as_device_f32(rotations, self.device)
+        if tuple(pos.shape) != (n, b, 3) or tuple(rot.shape) != (n, b, 4):
+            raise ValueError(f"expected poses shaped {(n, b, 3)} / {(n, b, 4)}, "
+                             f"got {tuple(pos.shape)} / {tuple(rot.shape)}")
+        if validate and pos.numel():
+            finite = torch.isfinite(pos).all() & torch.isfinite(rot).all()
+            small = (rot.double().norm(dim=-1) < 1e-12).any()
+            ok, zero = bool(finite.item()), bool(small.item())
+            if not ok:
+                raise ValueError("poses must be finite")
+            if zero:
+                raise ValueError("zero quaternion in body rotations")
+        self.body_positions.copy_(pos)
+        self.body_rotations.copy_(rot)
+
+    def body_pose(self, env: int, body: int) -> RigidPose:
+        return RigidPose(self.body_positions[env, body].double().cpu().numpy(),
+                         self.body_rotations[env, body].double().cpu().numpy())
+
+    # -- camera randomisation (scene.py:256-277) -----------------------------
+    def set_camera_randomization(self, offset_pos, offset_rot, fov_delta) -> None:
+        n, c = self.num_envs, self.num_cameras
+        p = _as_device_f32(offset_pos, self.device)
+        r = _as_device_f32(offset_rot, self.device)
+        f = _as_device_f32(fov_delta, self.device)
+        if tuple(p.shape) != (n, c, 3) or tuple(r.shape) != (n, c, 4) or tuple(f.shape) != (n, c):
+            raise ValueError("camera randomization arrays have wrong shapes")
+        self._rand_pos, self._rand_rot, self._rand_fov = p, r, f
+
+    def clear_camera_randomization(self) -> None:
+        self._rand_pos = self._rand_rot = self._rand_fov = None
+
+    # -- host-side views of the derived state (API parity) --------------------
+    def camera_world_poses(self) -> tuple[np.ndarray, np.ndarray]:
+        """(N,C,3), (N,C,4): parent pose o mount o offset, as the prologue computes it."""
+        from .transforms import quat_mul, quat_normalize, quat_rotate
+        bp = self.body_positions.double().cpu().numpy()
+        bq = self.body_rotations.double().cpu().numpy()
+        rp = None if self._rand_pos is None else self._rand_pos.double().cpu().numpy()
+        rq = None if self._rand_rot is None else self._rand_rot.double().cpu().numpy()
+        n, c = self.num_envs, self.num_cameras
+        pos, rot = np.empty((n, c, 3)), np.empty((n, c, 4))
+        for ci, cam in enumerate(self.cameras):
+            for e in range(n):
+                t, q = cam.mount.translation, cam.mount.rotation
+                if cam.parent_body is not None:
+                    pq = quat_normalize(bq[e, cam.parent_body])
+                    t, q = bp[e, cam.parent_body] + quat_rotate(pq, t), quat_mul(pq, q)
+                if rp is not None:
+                    t, q = t + quat_rotate(q, rp[e, ci]), quat_mul(q, quat_normalize(rq[e, ci]))
+                pos[e, ci], rot[e, ci] = t, q
+        return pos, rot
+
+    def ray_grids(self) -> tuple[np.ndarray, np.ndarray]:
+        """Host copy of the ray grids the device generates on the fly (scene.py:304-329)."""
+        if self._rand_fov is None:
+            g = [cam.ray_grid() for cam in self.cameras]
+            return np.stack([d for d, _ in g])[None], np.stack([s for _, s in g])[None]
+        fov = self._rand_fov.double().cpu().numpy()
+        n, c, h, w = self.frame_shape
+        dirs, scale = np.empty((n, c, h, w, 3)), np.empty((n, c, h, w))
+        for ci, cam in enumerate(self.cameras):
+            for e in range(n):
+                dirs[e, ci], scale[e, ci] = cam.with_fov_delta(float(fov[e, ci])).ray_grid()
+        return dirs, scale
+
+    # -- native step ---------------------------------------------------------
+    def _step_args(self, out: torch.Tensor, early_termination: bool) -> _native.StepArgs:
+        a = _native.StepArgs()
+        a.num_envs = self.num_envs
+        a.flags = _native.EARLY_TERMINATION if early_termination else 0
+        a.env_offset = self.env_offset
+        a.body_pos = self.body_positions.data_ptr() if self.num_bodies else None
+        a.body_rot = self.body_rotations.data_ptr() if self.num_bodies else None
+        if self._rand_pos is not None:
+            a.cam_off_pos = self._rand_pos.data_ptr()
+            a.cam_off_rot = self._rand_rot.data_ptr()
+            a.fov_delta = self._rand_fov.data_ptr()
+        a.ray_envs = 1
+        a.out = out.data_ptr()
+        return a
+
+    def _launch(self, args: _native.StepArgs) -> None:
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._ctx.render(args, stream)
+
+    def _new_frame(self, out):
+        if out is None:
+            return torch.empty(self.frame_shape, dtype=torch.float32, device=self.device)
+        if (not isinstance(out, torch.Tensor) or out.device != self.device or out.dtype != torch.float32
+                or tuple(out.shape) != self.frame_shape or not out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous float32 CUDA tensor of shape {self.frame_shape}")
+        return out
+
+
+def _check_backend(backend, threads):
+    from . import kernels
+    kernels.resolve_backend(backend)
+    if threads is not None:
+        kernels.resolve_threads(threads)
+
+
+def render(scene: Scene, *, early_termination: bool = True, backend: str | None = None,
+           threads: int | None = None, timestamp: float = 0.0, out=None,
+           counters: torch.Tensor | None = None) -> DepthFrame:
+    """One ray per (env, camera, pixel); returns range depth (scene.py:332-348).
+
+    Bodies are queried in their link frames (never rebuilt), then terrain in
+    the world frame bounded by the best body hit when early_termination is on.
+    ``counters`` (int64 CUDA tensor of 2) accumulates BVH node-record fetches
+    and triangle tests (the algorithmic-bytes denominator).
+    """
+    _check_backend(backend, threads)
+    data = scene._new_frame(out)
+    args = scene._step_args(data, early_termination)
+    if counters is not None:
+        args.flags |= _native.COUNT
+        args.counters = counters.data_ptr()
+    scene._launch(args)
+    return DepthFrame(data, timestamp)
+
+
+def render_naive_baseline(*args, **kwargs):
+    """The reference's refit-per-env baseline (scene.py:351-378) exists only
+    to be slow; the GPU renderer has no refit path to compare against."""
+    raise NotImplementedError("render_naive_baseline is a CPU benchmark foil; not provided on the GPU")
+
+
+def depth_to_z(frame, scale):
+    """range / |K^-1 p| (scene.py:381-387); works on numpy or torch."""
+    if isinstance(frame, torch.Tensor):
+        return frame / torch.as_tensor(scale, dtype=frame.dtype, device=frame.device)
+    return np.asarray(frame) / np.asarray(scale)

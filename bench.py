@@ -1,0 +1,459 @@
+"""Benchmark: depth rays/s of the multi-depth pipeline on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+One *step* = one pass of the hot path over one batch: for every env slice of
+this rank, camera poses from link poses (prologue), a ray per (env, cam,
+pixel) through the G1-proxy link BVHs (link frames) and the terrain BVH, the
+sensor model (noise, dropout, clamp) and the latency ring write + delayed
+read -- i.e. ``render_pipeline`` (render -> apply_noise_dropout ->
+FrameBuffer.push -> fetch_delayed_batch of the reference).
+
+Default workload = config 2 of BASELINE.json: 4096 envs x 2 cams x 64x48 per
+GPU (weak scaling; 8 GPUs = config 4's 32768 envs), 259,200-triangle
+slope/stairs tile field, 30-link G1 proxy, full noise/dropout/latency.
+
+``value``: rays/s with inputs resident in HBM (per-step device pose update +
+pipeline), CUDA-event timed per step with an L2 flush (256 MiB write) between
+steps. ``e2e``: the same through the public API with host buffers: pinned
+host poses -> H2D, pipeline, D2H of the observation, every step.
+``--impl reference``: the CPU restatement of the reference path
+(oracle/oracle.c, OpenMP on all host cores) on a bounded env sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "depth rays/sec at 4096 envs x 2 cams, 1/2/4/8 B200; % of L2/HBM BW roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default: config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--pose-sets", type=int, default=8)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def f32(x):
+    return np.asarray(x, np.float64).astype(np.float32)
+
+
+def cfg_envs(name):
+    return {"cfg2": 4096, "cfg3": 4096, "cfg5": 4096}[name]
+
+
+def workload_desc(name):
+    return {
+        "cfg2": "4096 envs x 2 cams (front+back) 64x48 per GPU, 3x3 slope/stairs tiles (259,200 tris), "
+                "30-link G1 proxy (8,060 tris), full noise/dropout/latency",
+        "cfg3": "4096 envs x 4 cams 64x48, stepping stones 25cm/60cm (8,750 tris), arms raised, full sensor",
+        "cfg5": "4096 envs x 2 cams 160x120, 708x708-node rolling terrain (999,698 tris), full sensor",
+    }[name]
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampler during the timed region)
+# ---------------------------------------------------------------------------
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, nm in REASON_BITS.items():
+                if bits & b and nm != "gpu_idle":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle restatement on host cores
+# ---------------------------------------------------------------------------
+
+def build_oracle_workload(name, n_sample, world_envs):
+    from oracle import oracle as orc
+    from paper_2602_03002_b200 import synth, sensor
+    w = synth.config(name, world_envs)
+    bodies = [(f32(m.vertices).astype(np.float64), m.faces) for _, m in w.bodies]
+    terrain = (f32(w.terrain.mesh.vertices).astype(np.float64), w.terrain.mesh.faces)
+    cams = [dict(width=c.width, height=c.height, hfov_deg=c.hfov_deg, vfov_deg=c.vfov_deg, d_max=c.d_max,
+                 mount_pos=c.mount.translation, mount_rot=c.mount.rotation, parent=c.parent_body)
+            for c in w.cameras]
+    sc = orc.OracleScene(bodies, terrain, cams)
+    return orc, w, sc
+
+
+def run_cpu_sample(orc, w, sc, n_sample, step, threads, buf_state, delays, cfg):
+    """render + apply_noise_dropout + FrameBuffer push/fetch on n_sample envs (oracle port)."""
+    sl = slice(0, n_sample)
+    bp, bq = w.poses(step, sl)
+    bp, bq = f32(bp).astype(np.float64), f32(bq).astype(np.float64)
+    depth = sc.render(bp, bq, threads=threads)
+    dmax = np.array([c["d_max"] for c in sc.cameras])
+    noisy = orc.apply_noise_dropout(depth, noise_scale=cfg.noise_scale, dropout_p=cfg.dropout_p, seed=cfg.seed,
+                                    d_max=dmax, step=step, threads=threads)
+    times, frames = buf_state
+    times.append(step * 0.02)
+    frames.append(noisy)
+    if len(times) > 8:
+        times.pop(0)
+        frames.pop(0)
+    idx = orc.frame_select(np.array(times), step * 0.02, delays[:n_sample])
+    obs = np.stack([frames[k][e] for e, k in enumerate(idx)])
+    return obs
+
+
+def cpu_measure(name, steps, warmup, seconds_target, threads):
+    """Returns (rays_per_s, sample_desc, per-step list)."""
+    from paper_2602_03002_b200 import sensor
+    cfg = sensor.SensorConfig(noise_scale=0.1, dropout_p=0.05, seed=0)
+    probe_n = 16
+    orc, w, sc = build_oracle_workload(name, probe_n, cfg_envs(name))
+    delays = sensor.sample_latencies(sensor.SensorConfig(max_delay=0.1, seed=3), w.num_envs)
+    rays_per_env = len(w.cameras) * w.cameras[0].width * w.cameras[0].height
+    # size the sample so each step costs ~seconds_target / steps
+    state = ([], [])
+    t0 = time.perf_counter()
+    run_cpu_sample(orc, w, sc, probe_n, 0, threads, state, delays, cfg)
+    per_env = (time.perf_counter() - t0) / probe_n
+    n_sample = int(max(8, min(w.num_envs, seconds_target / max(steps, 1) / max(per_env, 1e-6))))
+    state = ([], [])
+    for s in range(warmup):
+        run_cpu_sample(orc, w, sc, n_sample, s, threads, state, delays, cfg)
+    times = []
+    for s in range(steps):
+        t0 = time.perf_counter()
+        run_cpu_sample(orc, w, sc, n_sample, warmup + s, threads, state, delays, cfg)
+        times.append(time.perf_counter() - t0)
+    rays = n_sample * rays_per_env
+    value = rays * len(times) / sum(times)
+    desc = (f"{n_sample} of {w.num_envs} envs x {len(w.cameras)} cams x {w.cameras[0].width}x"
+            f"{w.cameras[0].height} per step (render + noise/dropout + latency), {len(times)} steps")
+    return value, desc, times
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    threads = orc.max_threads()
+    value, desc, _ = cpu_measure(args.config, args.steps, args.warmup, args.cpu_seconds * 3, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config), "impl_detail": "oracle/oracle.c (C restatement of "
+                   "multidepth numba_backend._render_kernel + sensor + FrameBuffer), OpenMP"},
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "port", "sample": desc,
+                         "cpu": cpu_info()},
+        "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+    import paper_2602_03002_b200 as md
+    from paper_2602_03002_b200 import _native, synth
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = args.envs or cfg_envs(args.config)
+    total_envs = n * world
+    w = synth.config(args.config, total_envs)
+    env0 = rank * n
+    bodies = [(nm, md.TriMesh(f32(m.vertices).astype(np.float64), m.faces, frame="body-local"))
+              for nm, m in w.bodies]
+    terrain = md.TriMesh(f32(w.terrain.mesh.vertices).astype(np.float64), w.terrain.mesh.faces)
+    t_build = time.perf_counter()
+    scene = md.Scene(n, bodies=bodies, cameras=w.cameras, terrain=terrain, device=dev, env_offset=env0)
+    t_build = time.perf_counter() - t_build
+    C, H, W = scene.num_cameras, scene.height, scene.width
+    rays_per_step = n * C * H * W
+
+    # camera randomisation + latency per env (global counters, sliced to this rank)
+    off = md.sample_camera_offsets(md.CameraRandomization(seed=3), total_envs, C)
+    scene.set_camera_randomization(*(np.asarray(a)[env0:env0 + n] for a in off))
+    sens = md.SensorConfig(noise_scale=0.1, dropout_p=0.05, max_delay=0.1, seed=0)
+    delays_np = md.sample_latencies(md.SensorConfig(max_delay=0.1, seed=3), total_envs)[env0:env0 + n]
+    delays = torch.from_numpy(np.ascontiguousarray(delays_np)).to(dev)
+    dt = 0.02
+
+    # per-step link poses: P distinct sets (host FK once), device-resident and pinned-host copies
+    P = args.pose_sets
+    pose_host = []
+    for s in range(P):
+        p, q = w.poses(s, slice(env0, env0 + n))
+        pose_host.append((torch.from_numpy(f32(p)).pin_memory(), torch.from_numpy(f32(q)).pin_memory()))
+    pose_dev = [(p.to(dev), q.to(dev)) for p, q in pose_host]
+
+    buf = md.FrameBuffer(capacity=8)
+    out = torch.empty(scene.frame_shape, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    step_id = [0]
+
+    def step(poses):
+        s = step_id[0]
+        scene.set_body_poses(poses[0], poses[1], validate=False)
+        md.render_pipeline(scene, sensor=sens, step=s, frame_buffer=buf, timestamp=s * dt, delays=delays,
+                           out=out)
+        step_id[0] += 1
+
+    # ---- per-ray work counts (untimed, MDRT_COUNT) ----
+    ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+    scene.set_body_poses(*pose_dev[0], validate=False)
+    md.render(scene, counters=ctr)
+    torch.cuda.synchronize()
+    nodes_per_ray, tris_per_ray = (x / rays_per_step for x in ctr.tolist())
+
+    for i in range(args.warmup):
+        step(pose_dev[i % P])
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident inputs ----
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        starts[i].record(stream)
+        step(pose_dev[i % P])
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+
+    # ---- render-kernel-only timing (roofline of the dominant kernel) ----
+    kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kend = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        s = step_id[0]
+        scene.set_body_poses(*pose_dev[i % P], validate=False)
+        a = scene._step_args(out, True)
+        a.flags |= _native.PHASE_PROLOGUE
+        scene._launch(a)
+        flush.fill_(float(i))
+        a = scene._step_args(out, True)
+        a.flags |= _native.PHASE_TRACE | _native.SENSOR
+        a.noise_scale, a.dropout_p, a.sensor_key, a.step = sens.noise_scale, sens.dropout_p, sens.key, s
+        kstart[i].record(stream)
+        scene._launch(a)
+        kend[i].record(stream)
+        step_id[0] += 1
+    torch.cuda.synchronize()
+    kernel_ms = statistics.mean(s.elapsed_time(e) for s, e in zip(kstart, kend))
+
+    # ---- L2 read bandwidth probe (roofline denominator for L2-resident traversal) ----
+    l2_gbs = None
+    try:
+        import ctypes
+        pb = torch.empty(32 * 1024 * 1024 // 4, dtype=torch.float32, device=dev).fill_(1.0)
+        sink = torch.empty(8192, dtype=torch.float32, device=dev)
+        L = _native.lib()
+        L.mdrt_probe_read(ctypes.c_void_p(pb.data_ptr()), pb.numel() * 4, 4, ctypes.c_void_p(sink.data_ptr()),
+                          ctypes.c_void_p(stream.cuda_stream))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        iters = 50
+        _native.check(L.mdrt_probe_read(ctypes.c_void_p(pb.data_ptr()), pb.numel() * 4, iters,
+                                        ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        l2_gbs = pb.numel() * 4 * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    except Exception as exc:  # probe is diagnostic only
+        print(f"l2 probe failed: {exc}", file=sys.stderr)
+
+    # ---- e2e: public API with host buffers (H2D poses, D2H observation) ----
+    host_obs = torch.empty(scene.frame_shape, dtype=torch.float32).pin_memory()
+    e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        e_starts[i].record(stream)
+        hp, hq = pose_host[i % P]
+        scene.set_body_poses(hp, hq, validate=False)        # pinned host -> device
+        obs = md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf,
+                                 timestamp=step_id[0] * dt, delays=delays, out=out)
+        host_obs.copy_(obs, non_blocking=True)              # device -> pinned host
+        e_ends[i].record(stream)
+        step_id[0] += 1
+    torch.cuda.synchronize()
+    e2e_ms = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends))
+    h2d = pose_host[0][0].numel() * 4 + pose_host[0][1].numel() * 4
+    d2h = host_obs.numel() * 4
+
+    # max over ranks
+    tt = torch.tensor([total_ms, e2e_ms, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms, e2e_ms, kernel_ms = tt.tolist()
+
+    if rank == 0:
+        all_rays = rays_per_step * world * args.steps
+        value = all_rays / (total_ms * 1e-3)
+        e2e_value = all_rays / (e2e_ms * 1e-3)
+        # algorithmic bytes of one render-kernel launch (this rank's slice)
+        node_b, tri_b = 64, 48
+        warps = n * C * math.ceil(W / 8) * math.ceil(H / 4)
+        lag_frac = float(np.mean(delays_np >= dt))    # envs reading an older ring slot
+        io_b = 4 + 4 + 4 * lag_frac                   # ring write + obs write + delayed read
+        bytes_per_ray = nodes_per_ray * node_b + tris_per_ray * tri_b + io_b
+        launch_bytes = rays_per_step * bytes_per_ray + warps * 128
+        achieved = launch_bytes / (kernel_ms * 1e-3) / 1e9
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            from oracle import oracle as orc
+            th = orc.max_threads()
+            cv, cdesc, _ = cpu_measure(args.config, 3, 1, args.cpu_seconds, th)
+            cpu = {"value": cv, "unit": "rays/s", "cores": th, "kind": "port", "sample": cdesc, "cpu": cpu_info()}
+        line = {
+            "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config), "envs_per_gpu": n, "cams": C,
+                       "resolution": f"{W}x{H}", "global_envs": total_envs,
+                       "parallelism": f"env-slice x{world} (replicated BVHs, no collective in the step)",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "terrain_tris": scene.geometry_stats["terrain_triangles"],
+                       "body_tris": scene.geometry_stats["body_triangles"],
+                       "bvh_bytes": scene.geometry_stats["node_bytes"] + scene.geometry_stats["tri_bytes"],
+                       "build_s": round(t_build, 3)},
+            "frames_per_s": value / (H * W),
+            "steps_per_s": 1e3 / (total_ms / args.steps),
+            "per_ray": {"node_fetches": nodes_per_ray, "tri_tests": tris_per_ray, "bytes": bytes_per_ray,
+                        "node_record_b": node_b, "tri_record_b": tri_b, "io_b": io_b},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "render_kernel (K1+K2+K3 fused)", "kernel_ms": kernel_ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                         "l2_probe_gbs": l2_gbs,
+                         "l2_frac": (achieved / l2_gbs) if l2_gbs else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk,
+            "wall_s_timed": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

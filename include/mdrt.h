@@ -40,6 +40,8 @@ extern "C" {
 #define MDRT_LATENCY 0x4           /* fused latency ring write + delayed read (sensor.py:103-150)   */
 #define MDRT_COUNT 0x8             /* count BVH node visits / triangle tests into `counters`         */
 #define MDRT_NO_CULL 0x10          /* disable per-view link culling (debug / A-B parity)            */
+#define MDRT_PHASE_PROLOGUE 0x20   /* launch only the per-view prologue (timing); neither phase flag = both */
+#define MDRT_PHASE_TRACE 0x40      /* launch only the traversal kernel (uses the last prologue's records)  */
 
 typedef struct mdrt_ctx mdrt_ctx;
 
@@ -168,6 +170,11 @@ int mdrt_downsample_min(const float *in, float *out, int64_t planes, int32_t H, 
  * MDRT_EINVAL with a message when an invariant fails. */
 int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_t nf,
                    int64_t info[4]);
+
+/* Bandwidth probe for roofline denominators: `iters` passes of 16-byte loads
+ * over a device buffer of `bytes` (L2-resident when bytes << L2 size); writes
+ * one float per block into `sink` (device, >= 4096 floats) so loads are live. */
+int mdrt_probe_read(const void *buf, int64_t bytes, int32_t iters, float *sink, void *stream);
 
 /* Synchronise the context's device (debug/tests). */
 int mdrt_sync(mdrt_ctx *ctx);

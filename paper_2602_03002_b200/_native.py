@@ -24,6 +24,8 @@ SENSOR = 0x2
 LATENCY = 0x4
 COUNT = 0x8
 NO_CULL = 0x10
+PHASE_PROLOGUE = 0x20
+PHASE_TRACE = 0x40
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -119,6 +121,7 @@ def lib():
             "mdrt_downsample_min": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                                    ctypes.c_int32, vp]),
             "mdrt_bvh_check": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64, _c_i64p]),
+            "mdrt_probe_read": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp]),
             "mdrt_sync": (ctypes.c_int, [vp]),
         }
         for name, (res, args) in sig.items():
@@ -133,7 +136,7 @@ def lib():
 EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_create", "mdrt_destroy",
            "mdrt_add_body", "mdrt_set_terrain", "mdrt_set_cameras", "mdrt_commit", "mdrt_get_stats",
            "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
-           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_sync")
+           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_sync")
 
 
 def check(rc: int) -> None:

@@ -351,8 +351,13 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         }
         pp.views = ctx->views.ptr;
         pp.links = ctx->links.ptr;
-        launch_prologue(pp, static_cast<int64_t>(nviews), s);
-        CK(cudaGetLastError());
+        const bool only_pro = (a->flags & MDRT_PHASE_PROLOGUE) && !(a->flags & MDRT_PHASE_TRACE);
+        const bool only_trace = (a->flags & MDRT_PHASE_TRACE) && !(a->flags & MDRT_PHASE_PROLOGUE);
+        if (!only_trace) {
+            launch_prologue(pp, static_cast<int64_t>(nviews), s);
+            CK(cudaGetLastError());
+        }
+        if (only_pro) return;
 
         RenderParams rp{};
         rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
@@ -524,6 +529,14 @@ int mdrt_bvh_check(const double* verts, int64_t nv, const int64_t* faces, int64_
         info[1] = static_cast<int64_t>(t.tris.size());
         info[2] = maxd;
         info[3] = leaves;
+    });
+}
+
+int mdrt_probe_read(const void* buf, int64_t bytes, int32_t iters, float* sink, void* stream) {
+    return guarded([&] {
+        need(buf && sink && bytes >= 16 && iters >= 1, "bad probe arguments");
+        launch_probe_read(static_cast<const float4*>(buf), bytes / 16, iters, sink, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
     });
 }
 

@@ -397,6 +397,28 @@ static __global__ void downsample_kernel(DownsampleParams p) {
     p.out[i] = mn;
 }
 
+// read-bandwidth probe: grid-stride 16 B loads, one partial sum per block
+static __global__ void __launch_bounds__(256) probe_read_kernel(const float4* __restrict__ buf, int64_t n16,
+                                                                int iters, float* sink) {
+    float acc = 0.f;
+    for (int it = 0; it < iters; ++it) {
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const float4 v = __ldcg(buf + i);
+            acc += (v.x + v.y) + (v.z + v.w);
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    __shared__ float s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < 8; ++w) t += s[w];
+        sink[blockIdx.x] = t;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -425,6 +447,13 @@ void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s) {
 
 void launch_select(const SelectParams& p, int64_t n, cudaStream_t s) {
     select_kernel<<<grid_for(n, 256), 256, 0, s>>>(p);
+}
+
+void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    probe_read_kernel<<<sms * 8, 256, 0, s>>>(buf, n16, iters, sink);
 }
 
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s) {

@@ -43,7 +43,7 @@ METRIC = "depth rays/sec at 4096 envs x 2 cams, 1/2/4/8 B200; % of L2/HBM BW roo
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

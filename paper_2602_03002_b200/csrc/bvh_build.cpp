@@ -92,8 +92,8 @@ class Builder {
         int64_t mid = -1;
         // Switch to object-median splits when the remaining depth budget gets
         // tight: a median tree below this node adds ceil(log2(n)) levels.
-        int need = 1;
-        while ((int64_t(1) << need) < n) ++need;
+        int need = 0;
+        while ((int64_t(kMaxLeafTris) << need) < n) ++need;
         const bool force_median = depth + need + 1 >= kMaxDepth;
         if (!force_median) {
             double best_cost = std::numeric_limits<double>::infinity();
@@ -310,7 +310,11 @@ PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int
 
     // bounding sphere of the vertices actually referenced
     Box all = root.box;
-    for (int a = 0; a < 3; ++a) out.center[a] = 0.5 * (all.lo[a] + all.hi[a]);
+    for (int a = 0; a < 3; ++a) {
+        out.center[a] = 0.5 * (all.lo[a] + all.hi[a]);
+        out.box_lo[a] = all.lo[a];
+        out.box_hi[a] = all.hi[a];
+    }
     double r2 = 0.0;
     for (int64_t f = 0; f < nf; ++f)
         for (int k = 0; k < 3; ++k) {

@@ -31,7 +31,7 @@ struct alignas(16) PackedTri {
 static_assert(sizeof(PackedTri) == 48, "triangle record must be 48 B");
 
 constexpr int kMaxLeafTris = 4;
-constexpr int kMaxDepth = 32;   // builder guarantees leaf depth <= kMaxDepth (= GPU stack size)
+constexpr int kMaxDepth = 24;   // builder guarantees leaf depth <= kMaxDepth (= GPU stack size)
 
 inline int32_t leaf_ref(int64_t first, int count) {
     return ~static_cast<int32_t>((first << 3) | (count - 1));
@@ -44,6 +44,8 @@ struct PackedTree {
     int depth = 0;                   // max leaf depth (root = 0)
     double center[3] = {0, 0, 0};    // bounding sphere (local frame)
     double radius = 0;
+    double box_lo[3] = {0, 0, 0};    // exact AABB of the referenced vertices (local frame)
+    double box_hi[3] = {0, 0, 0};
 };
 
 // Build + pack one mesh. verts (nv,3) f64, faces (nf,3) i64. Faces must be

@@ -112,6 +112,7 @@ struct mdrt_ctx {
     // per-step scratch
     DevBuf<ViewRec> views;
     DevBuf<LinkRec> links;
+    DevBuf<unsigned int> tile_counter;
 
     void use_device() const { CK(cudaSetDevice(device)); }
 };
@@ -157,6 +158,7 @@ int mdrt_destroy(mdrt_ctx* ctx) {
         ctx->rig_buf.release();
         ctx->views.release();
         ctx->links.release();
+        ctx->tile_counter.release();
         delete ctx;
     });
 }
@@ -250,6 +252,10 @@ int mdrt_commit(mdrt_ctx* ctx) {
             bi.cy = static_cast<float>(b.center[1]);
             bi.cz = static_cast<float>(b.center[2]);
             bi.r = static_cast<float>(b.radius * (1.0 + 1e-6)) + 1e-5f;
+            // padded half extents of the link AABB around the sphere centre
+            bi.hx = static_cast<float>(0.5 * (b.box_hi[0] - b.box_lo[0]) * (1.0 + 1e-5) + 1e-4);
+            bi.hy = static_cast<float>(0.5 * (b.box_hi[1] - b.box_lo[1]) * (1.0 + 1e-5) + 1e-4);
+            bi.hz = static_cast<float>(0.5 * (b.box_hi[2] - b.box_lo[2]) * (1.0 + 1e-5) + 1e-4);
             infos.push_back(bi);
             st.body_nodes += static_cast<int64_t>(b.nodes.size());
             st.body_triangles += static_cast<int64_t>(b.tris.size());
@@ -384,8 +390,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.out_clean = a->out_clean;
         rp.out = a->out;
         rp.counters = a->counters;
+        ctx->tile_counter.reserve(1);
+        rp.tile_counter = ctx->tile_counter.ptr;
         const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;
-        need((warps * 32 + kBlock - 1) / kBlock < (int64_t(1) << 31), "launch too large");
+        need(warps < (int64_t(1) << 31), "launch too large");
         launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, s);
         CK(cudaGetLastError());
     });

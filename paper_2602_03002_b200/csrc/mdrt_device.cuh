@@ -11,7 +11,7 @@
 
 namespace mdrt {
 
-constexpr int kStack = 32;          // == kMaxDepth of the builder
+constexpr int kStack = 24;          // == kMaxDepth of the builder
 constexpr int kBlock = 128;         // threads per render block (4 warps, 4 tiles)
 constexpr int kTileW = 8;           // a warp renders an 8x4 pixel tile of one view
 constexpr int kTileH = 4;
@@ -28,11 +28,12 @@ struct CamRig {
     int32_t pad;
 };
 
-// Per-body constants: tree root and local-frame bounding sphere.
+// Per-body constants: tree root, local-frame bounding sphere and box (centre cx..cz,
+// half extents hx..hz, padded outward).
 struct alignas(16) BodyInfo {
     float cx, cy, cz, r;
+    float hx, hy, hz;
     int32_t root;
-    int32_t pad[3];
 };
 
 // Per-(env,cam) view record written by the prologue (128 B).
@@ -116,19 +117,44 @@ struct TraceCounters {
     unsigned int tris = 0;
 };
 
+// Approximate reciprocal (MUFU.RCP, <= 1 ulp): slab and triangle tests only
+// need it to within the builder's conservative box padding (bvh_build.cpp).
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 // Returns the nearest hit parameter t in (1e-6, tmax] or +inf when nothing
 // is hit (the caller then keeps its bound; numba_backend.py:206-208).
-// `stack` points at this thread's column of a [kStack][kBlock] shared array.
+// Ordered closest-hit traversal: at an inner record both child boxes are
+// slab-tested, the nearer hit child is descended and the farther one pushed
+// together with its entry distance, so pops whose entry lies beyond the best
+// hit so far are discarded without fetching the record.
+// `stack_ref`/`stack_t` point at this thread's column of [kStack][kBlock] shared arrays.
 template <bool COUNT>
 __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                        int32_t root, float ox, float oy, float oz, float dx, float dy,
-                                       float dz, float tmax, int* __restrict__ stack, TraceCounters& ctr) {
+                                       float dz, float tmax, int* __restrict__ stack_ref,
+                                       float* __restrict__ stack_t, TraceCounters& ctr) {
     // zero direction components: a huge reciprocal turns the slab into a
     // containment test like _slab_hit's d == 0 branch (numba_backend.py:76-78)
     const float tiny = 1e-30f;
-    const float idx = 1.0f / (fabsf(dx) > tiny ? dx : copysignf(tiny, dx));
-    const float idy = 1.0f / (fabsf(dy) > tiny ? dy : copysignf(tiny, dy));
-    const float idz = 1.0f / (fabsf(dz) > tiny ? dz : copysignf(tiny, dz));
+    const float idx = rcp_approx(fabsf(dx) > tiny ? dx : copysignf(tiny, dx));
+    const float idy = rcp_approx(fabsf(dy) > tiny ? dy : copysignf(tiny, dy));
+    const float idz = rcp_approx(fabsf(dz) > tiny ? dz : copysignf(tiny, dz));
     const float oxd = ox * idx, oyd = oy * idy, ozd = oz * idz;
 
     float best = tmax;
@@ -146,27 +172,32 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             const float a0 = fmaf(bx.x, idx, -oxd), a1 = fmaf(bx.y, idx, -oxd);
             const float a2 = fmaf(bx.z, idy, -oyd), a3 = fmaf(bx.w, idy, -oyd);
             const float a4 = fmaf(bz.x, idz, -ozd), a5 = fmaf(bz.y, idz, -ozd);
-            const float c0min = fmaxf(fmaxf(fminf(a0, a1), fminf(a2, a3)), fmaxf(fminf(a4, a5), 0.0f));
-            const float c0max = fminf(fminf(fmaxf(a0, a1), fmaxf(a2, a3)), fminf(fmaxf(a4, a5), best));
+            const float c0min = fmax3(fminf(a0, a1), fminf(a2, a3), fmaxf(fminf(a4, a5), 0.0f));
+            const float c0max = fmin3(fmaxf(a0, a1), fmaxf(a2, a3), fminf(fmaxf(a4, a5), best));
             const float b0 = fmaf(by.x, idx, -oxd), b1 = fmaf(by.y, idx, -oxd);
             const float b2 = fmaf(by.z, idy, -oyd), b3 = fmaf(by.w, idy, -oyd);
             const float b4 = fmaf(bz.z, idz, -ozd), b5 = fmaf(bz.w, idz, -ozd);
-            const float c1min = fmaxf(fmaxf(fminf(b0, b1), fminf(b2, b3)), fmaxf(fminf(b4, b5), 0.0f));
-            const float c1max = fminf(fminf(fmaxf(b0, b1), fmaxf(b2, b3)), fminf(fmaxf(b4, b5), best));
+            const float c1min = fmax3(fminf(b0, b1), fminf(b2, b3), fmaxf(fminf(b4, b5), 0.0f));
+            const float c1max = fmin3(fmaxf(b0, b1), fmaxf(b2, b3), fminf(fmaxf(b4, b5), best));
             const bool h0 = c0min <= c0max;
             const bool h1 = c1min <= c1max;
             if (h0 && h1) {
-                int32_t near = rf.x, far = rf.y;
-                if (c1min < c0min) { near = rf.y; far = rf.x; }
-                stack[sp * kBlock] = far;
+                const bool swap = c1min < c0min;
+                stack_ref[sp * kBlock] = swap ? rf.x : rf.y;
+                stack_t[sp * kBlock] = swap ? c0min : c1min;
                 ++sp;
-                ref = near;
-            } else if (h0) {
-                ref = rf.x;
-            } else if (h1) {
-                ref = rf.y;
+                ref = swap ? rf.y : rf.x;
+            } else if (h0 || h1) {
+                ref = h0 ? rf.x : rf.y;
             } else {
-                ref = sp > 0 ? stack[(--sp) * kBlock] : kExit;
+                ref = kExit;
+                while (sp > 0) {
+                    --sp;
+                    if (stack_t[sp * kBlock] <= best) {
+                        ref = stack_ref[sp * kBlock];
+                        break;
+                    }
+                }
             }
         }
         if (ref == kExit) break;
@@ -185,7 +216,7 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             const float py = dz * e2.x - dx * e2.z;
             const float pz = dx * e2.y - dy * e2.x;
             const float det = e1.x * px + e1.y * py + e1.z * pz;
-            const float inv = 1.0f / det;
+            const float inv = rcp_approx(det);
             const float tx = ox - v0.x, ty = oy - v0.y, tz = oz - v0.z;
             const float u = (tx * px + ty * py + tz * pz) * inv;
             const float qx = ty * e1.z - tz * e1.y;
@@ -200,7 +231,14 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
                 hit = true;
             }
         }
-        ref = sp > 0 ? stack[(--sp) * kBlock] : kExit;
+        ref = kExit;
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp * kBlock] <= best) {
+                ref = stack_ref[sp * kBlock];
+                break;
+            }
+        }
         if (ref == kExit) break;
     }
     return hit ? best : __int_as_float(0x7f800000);

@@ -13,6 +13,7 @@
 //                          sensor-stage operators (sensor.py:55-150).
 #include "mdrt_kernels.h"
 
+#include <algorithm>
 #include <cmath>
 
 namespace mdrt {
@@ -52,18 +53,6 @@ __device__ __forceinline__ void qmat(Q q, double m[9]) {
     m[0] = 1 - 2 * (y * y + z * z); m[1] = 2 * (x * y - w * z);     m[2] = 2 * (x * z + w * y);
     m[3] = 2 * (x * y + w * z);     m[4] = 1 - 2 * (x * x + z * z); m[5] = 2 * (y * z - w * x);
     m[6] = 2 * (x * z - w * y);     m[7] = 2 * (y * z + w * x);     m[8] = 1 - 2 * (x * x + y * y);
-}
-
-// Conservative range of slopes s = a/Z of rays through the origin that touch a
-// circle of radius r centred at (A, Z) (projection of the link sphere).
-__device__ __forceinline__ bool slope_range(double A, double Z, double r, double& lo, double& hi) {
-    const double den = Z * Z - r * r;
-    const double disc = A * A + Z * Z - r * r;
-    if (!(den > 0.0) || !(disc > 0.0)) return false;  // unbounded -> caller uses full range
-    const double s = sqrt(disc);
-    lo = (A * Z - r * s) / den;
-    hi = (A * Z + r * s) / den;
-    return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -144,17 +133,57 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
             keep = (dist - r) <= rig.d_max * (1.0 + 1e-6) + 1e-6;
             int x0 = 0, x1 = p.W - 1, y0 = 0, y1 = p.H - 1;
             if (keep && !grid && !p.no_cull) {
-                keep = Z + r > 0.0;  // every ray point with t > 0 has camera z = t > 0
-                double lo, hi;
-                if (keep && Z - r > 1e-9 && slope_range(X, Z, r, lo, hi)) {
-                    x0 = max(x0, static_cast<int>(floor(lo * fx + cx - 0.5)) - 1);
-                    x1 = min(x1, static_cast<int>(ceil(hi * fx + cx - 0.5)) + 1);
+                // Project the link box (clipped at the hit plane z = 1e-6; camera-frame
+                // rays are (u, v, 1) so z == t) to a conservative pixel rectangle.
+                double A[3][3];  // camera-frame half-axis vectors of the box
+                const double hk[3] = {bi.hx, bi.hy, bi.hz};
+                for (int kx = 0; kx < 3; ++kx) {
+                    const double lx = L[0 * 3 + kx] * hk[kx], ly = L[1 * 3 + kx] * hk[kx], lz = L[2 * 3 + kx] * hk[kx];
+                    A[kx][0] = R[0] * lx + R[3] * ly + R[6] * lz;
+                    A[kx][1] = R[1] * lx + R[4] * ly + R[7] * lz;
+                    A[kx][2] = R[2] * lx + R[5] * ly + R[8] * lz;
                 }
-                if (keep && Z - r > 1e-9 && slope_range(Y, Z, r, lo, hi)) {
-                    y0 = max(y0, static_cast<int>(floor(lo * fy + cy - 0.5)) - 1);
-                    y1 = min(y1, static_cast<int>(ceil(hi * fy + cy - 0.5)) + 1);
+                double cx3[8][3];
+                for (int q = 0; q < 8; ++q) {
+                    const double s0 = (q & 1) ? 1.0 : -1.0, s1 = (q & 2) ? 1.0 : -1.0, s2 = (q & 4) ? 1.0 : -1.0;
+                    for (int a = 0; a < 3; ++a)
+                        cx3[q][a] = (a == 0 ? X : a == 1 ? Y : Z) + s0 * A[0][a] + s1 * A[1][a] + s2 * A[2][a];
                 }
-                keep = keep && x0 <= x1 && y0 <= y1;
+                const double zc = 1e-6;
+                double sxlo = 1e300, sxhi = -1e300, sylo = 1e300, syhi = -1e300;
+                int front = 0;
+                auto add = [&](double px_, double py_, double pz_) {
+                    const double sx = px_ / pz_, sy = py_ / pz_;
+                    sxlo = fmin(sxlo, sx); sxhi = fmax(sxhi, sx);
+                    sylo = fmin(sylo, sy); syhi = fmax(syhi, sy);
+                };
+                for (int q = 0; q < 8; ++q) {
+                    if (cx3[q][2] > zc) { ++front; add(cx3[q][0], cx3[q][1], cx3[q][2]); }
+                }
+                keep = front > 0;
+                if (keep && front < 8) {
+                    // edges crossing the clip plane contribute their crossing point
+                    for (int q = 0; q < 8; ++q)
+                        for (int bit = 1; bit < 8; bit <<= 1) {
+                            const int q2 = q | bit;
+                            if (q2 == q) continue;
+                            const double z0 = cx3[q][2], z1 = cx3[q2][2];
+                            if ((z0 > zc) == (z1 > zc)) continue;
+                            const double f = (zc - z0) / (z1 - z0);
+                            add(cx3[q][0] + f * (cx3[q2][0] - cx3[q][0]), cx3[q][1] + f * (cx3[q2][1] - cx3[q][1]), zc);
+                        }
+                }
+                if (keep) {
+                    const double xl = sxlo * fx + cx - 0.5, xh = sxhi * fx + cx - 0.5;
+                    const double yl = sylo * fy + cy - 0.5, yh = syhi * fy + cy - 0.5;
+                    x0 = xl > x0 ? static_cast<int>(fmin(floor(xl) - 1.0, 1e9)) : x0;
+                    x1 = xh < x1 ? static_cast<int>(fmax(ceil(xh) + 1.0, -1e9)) : x1;
+                    y0 = yl > y0 ? static_cast<int>(fmin(floor(yl) - 1.0, 1e9)) : y0;
+                    y1 = yh < y1 ? static_cast<int>(fmax(ceil(yh) + 1.0, -1e9)) : y1;
+                    x0 = max(x0, 0); y0 = max(y0, 0);
+                    x1 = min(x1, p.W - 1); y1 = min(y1, p.H - 1);
+                    keep = x0 <= x1 && y0 <= y1;
+                }
             }
             if (keep) {
                 // M = L^T R (camera frame -> link frame), o = L^T (t - p)
@@ -223,22 +252,17 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
 // K1+K2+K3: render + fused sensor epilogue. One warp = one 8x4 tile of a view.
 // ---------------------------------------------------------------------------
 template <bool COUNT>
-static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p) {
-    __shared__ int s_stack[kStack * kBlock];
-    int* stack = s_stack + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) >> 5;
-    const int64_t total = static_cast<int64_t>(p.N) * p.C * p.tiles_per_view;
-    if (gw >= total) return;
-    const int64_t view = gw / p.tiles_per_view;
-    const int tile = static_cast<int>(gw - view * p.tiles_per_view);
-    const int ty = tile / p.tiles_x;
-    const int tx = tile - ty * p.tiles_x;
-    const int px = tx * kTileW + (lane & (kTileW - 1));
-    const int py = ty * kTileH + (lane >> 3);
+__device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int* stack,
+                                            float* stack_t) {
+    const uint32_t view = gw / static_cast<uint32_t>(p.tiles_per_view);
+    const uint32_t tile = gw - view * static_cast<uint32_t>(p.tiles_per_view);
+    const uint32_t ty = tile / static_cast<uint32_t>(p.tiles_x);
+    const uint32_t tx = tile - ty * static_cast<uint32_t>(p.tiles_x);
+    const int px = static_cast<int>(tx) * kTileW + (lane & (kTileW - 1));
+    const int py = static_cast<int>(ty) * kTileH + (lane >> 3);
     const bool active = px < p.W && py < p.H;
-    const int e = static_cast<int>(view / p.C);
-    const int c = static_cast<int>(view - static_cast<int64_t>(e) * p.C);
+    const uint32_t e = view / static_cast<uint32_t>(p.C);
+    const uint32_t c = view - e * static_cast<uint32_t>(p.C);
 
     const ViewRec& V = p.views[view];
     const float4 in = *reinterpret_cast<const float4*>(&V.ax);     // ax bx ay by
@@ -265,8 +289,9 @@ static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p
     float z = dmax;
 
     // ---- K2: links in their local frames (numba_backend.py:190-208) ----
+    const LinkRec* links = p.links + static_cast<int64_t>(view) * p.B;
     for (int k = 0; k < nlinks; ++k) {
-        const LinkRec& L = p.links[view * p.B + k];
+        const LinkRec& L = links[k];
         const int4 tail = *reinterpret_cast<const int4*>(&L.root);  // root | x0,x1 | y0,y1 | pad
         const int x0 = static_cast<int16_t>(tail.y & 0xffff), x1 = tail.y >> 16;
         const int y0 = static_cast<int16_t>(tail.z & 0xffff), y1 = tail.z >> 16;
@@ -281,7 +306,7 @@ static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p
             const float ldz = m1.z * dcx + m1.w * dcy + m2.x * dcz;
             const float bound = p.early_termination ? z : dmax;
             const float tt = trace<COUNT>(p.nodes, p.tris, tail.x, m2.y, m2.z, m2.w, ldx, ldy, ldz,
-                                          bound * inv_m, stack, ctr);
+                                          bound * inv_m, stack, stack_t, ctr);
             const float cand = m * tt;
             if (cand < z) z = cand;
         }
@@ -297,7 +322,7 @@ static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p
         const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
         const float bound = p.early_termination ? z : dmax;
         const float tt = trace<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
-                                      bound * inv_m, stack, ctr);
+                                      bound * inv_m, stack, stack_t, ctr);
         const float cand = m * tt;
         if (cand < z) z = cand;
     }
@@ -313,18 +338,22 @@ static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p
             atomicAdd(p.counters + 1, static_cast<unsigned long long>(nt));
         }
     }
-    if (!active) return;
 
     // ---- K3: fused epilogue ----
-    const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
-    if (p.out_clean) p.out_clean[o] = z;
     float val = z;
     if (p.sensor) {
-        const unsigned long long ru = absorb(V.hu, static_cast<unsigned long long>(py));
-        const unsigned long long rn = absorb(V.hn, static_cast<unsigned long long>(py));
+        // lanes 0-3 hash the tile's 4 rows of the uniform stream, lanes 4-7 of the
+        // normal stream; everyone picks its row's prefixes by shuffle
+        const unsigned long long rowh = absorb((lane & 4) ? V.hn : V.hu,
+                                               static_cast<unsigned long long>(ty * kTileH + (lane & 3)));
+        const unsigned long long ru = __shfl_sync(0xffffffffu, rowh, lane >> 3);
+        const unsigned long long rn = __shfl_sync(0xffffffffu, rowh, 4 + (lane >> 3));
         val = sensor_apply(z, ru, rn, static_cast<unsigned long long>(px), p.noise_scale, p.dropout_p,
                            p.fill[c], p.dmax64[c]);
     }
+    if (!active) return;
+    const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
+    if (p.out_clean) p.out_clean[o] = z;
     if (p.ring) {
         const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
         p.ring[static_cast<int64_t>(p.write_slot) * frame + o] = val;
@@ -334,6 +363,24 @@ static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p
     p.out[o] = val;
 }
 
+// Persistent warps: each warp pulls 8x4 tiles from a global counter until the
+// launch's tiles are exhausted (no block-tail idling, Aila & Laine style).
+template <bool COUNT>
+static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p) {
+    __shared__ int s_stack[kStack * kBlock];
+    __shared__ float s_stack_t[kStack * kBlock];
+    int* stack = s_stack + threadIdx.x;
+    float* stack_t = s_stack_t + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t total = static_cast<uint32_t>(p.N) * p.C * p.tiles_per_view;
+    while (true) {
+        uint32_t gw = 0;
+        if (lane == 0) gw = atomicAdd(p.tile_counter, 1u);
+        gw = __shfl_sync(0xffffffffu, gw, 0);
+        if (gw >= total) break;
+        render_tile<COUNT>(p, gw, lane, stack, stack_t);
+    }
+}
 
 // ---------------------------------------------------------------------------
 // standalone sensor-stage operators
@@ -431,10 +478,23 @@ void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s) {
 }
 
 void launch_render(const RenderParams& p, int64_t warps, bool count, cudaStream_t s) {
+    // persistent grid: as many blocks as can be co-resident (capped by the work)
+    static int blocks_per_sm[2] = {0, 0};
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], render_kernel<false>, kBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], render_kernel<true>, kBlock, 0);
+    }
+    const int64_t need = (warps * 32 + kBlock - 1) / kBlock;
+    const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(sms) * std::max(1, blocks_per_sm[count]));
+    cudaMemsetAsync(p.tile_counter, 0, sizeof(unsigned int), s);
     if (count)
-        render_kernel<true><<<grid_for(warps * 32, kBlock), kBlock, 0, s>>>(p);
+        render_kernel<true><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(p);
     else
-        render_kernel<false><<<grid_for(warps * 32, kBlock), kBlock, 0, s>>>(p);
+        render_kernel<false><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(p);
 }
 
 void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s) {

@@ -56,6 +56,7 @@ struct RenderParams {
     float* out_clean;
     float* out;
     unsigned long long* counters;
+    unsigned int* tile_counter;   // persistent-warp work counter (zeroed per launch)
 };
 
 struct NoiseParams {

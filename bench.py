@@ -293,11 +293,11 @@ def main():
         step_id[0] += 1
 
     # ---- per-ray work counts (untimed, MDRT_COUNT) ----
-    ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+    ctr = torch.zeros(4, dtype=torch.int64, device=dev)
     scene.set_body_poses(*pose_dev[0], validate=False)
     md.render(scene, counters=ctr)
     torch.cuda.synchronize()
-    nodes_per_ray, tris_per_ray = (x / rays_per_step for x in ctr.tolist())
+    nodes_per_ray, tris_per_ray, link_nodes_per_ray, link_traces_per_ray = (x / rays_per_step for x in ctr.tolist())
 
     for i in range(args.warmup):
         step(pose_dev[i % P])
@@ -435,6 +435,7 @@ def main():
             "frames_per_s": value / (H * W),
             "steps_per_s": 1e3 / (total_ms / args.steps),
             "per_ray": {"node_fetches": nodes_per_ray, "tri_tests": tris_per_ray, "bytes": bytes_per_ray,
+                        "link_node_fetches": link_nodes_per_ray, "link_traversals": link_traces_per_ray,
                         "node_record_b": node_b, "tri_record_b": tri_b, "io_b": io_b},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,

@@ -42,6 +42,7 @@ extern "C" {
 #define MDRT_NO_CULL 0x10          /* disable per-view link culling (debug / A-B parity)            */
 #define MDRT_PHASE_PROLOGUE 0x20   /* launch only the per-view prologue (timing); neither phase flag = both */
 #define MDRT_PHASE_TRACE 0x40      /* launch only the traversal kernel (uses the last prologue's records)  */
+#define MDRT_COUNT_DETAIL 0x80     /* with MDRT_COUNT: counters has 4 slots (+ link node fetches, link traversals) */
 
 typedef struct mdrt_ctx mdrt_ctx;
 
@@ -104,7 +105,7 @@ typedef struct {
 
     float *out_clean;          /* (N,C,H,W) clean range depth, or NULL                */
     float *out;                /* (N,C,H,W) final output (sensor/latency applied)     */
-    unsigned long long *counters; /* (2,) device [node visits, triangle tests] or NULL */
+    unsigned long long *counters; /* (2,) device [node fetches, triangle tests] or NULL; (4,) with MDRT_COUNT_DETAIL */
 } mdrt_step_args;
 
 /* ---- library ---------------------------------------------------------- */

@@ -26,6 +26,7 @@ COUNT = 0x8
 NO_CULL = 0x10
 PHASE_PROLOGUE = 0x20
 PHASE_TRACE = 0x40
+COUNT_DETAIL = 0x80
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)

@@ -390,6 +390,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.out_clean = a->out_clean;
         rp.out = a->out;
         rp.counters = a->counters;
+        rp.count_detail = (a->flags & MDRT_COUNT_DETAIL) != 0;
         ctx->tile_counter.reserve(1);
         rp.tile_counter = ctx->tile_counter.ptr;
         const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;

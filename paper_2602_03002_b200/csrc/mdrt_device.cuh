@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace mdrt {
@@ -115,6 +116,8 @@ __device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru
 struct TraceCounters {
     unsigned int nodes = 0;
     unsigned int tris = 0;
+    unsigned int link_nodes = 0;   // node fetches spent in link trees (subset of nodes)
+    unsigned int link_traces = 0;  // link traversals started
 };
 
 // Approximate reciprocal (MUFU.RCP, <= 1 ulp): slab and triangle tests only
@@ -123,6 +126,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
+}
+
+// 32-byte vector load through the non-coherent path (LDG.E.256 on sm_100a):
+// one 64 B node record = two requests instead of four LDG.128.
+__device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
 }
 
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
@@ -148,7 +159,7 @@ template <bool COUNT>
 __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                        int32_t root, float ox, float oy, float oz, float dx, float dy,
                                        float dz, float tmax, int* __restrict__ stack_ref,
-                                       float* __restrict__ stack_t, TraceCounters& ctr) {
+                                       __half* __restrict__ stack_t, TraceCounters& ctr) {
     // zero direction components: a huge reciprocal turns the slab into a
     // containment test like _slab_hit's d == 0 branch (numba_backend.py:76-78)
     const float tiny = 1e-30f;
@@ -164,10 +175,10 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
     while (true) {
         while (ref >= 0) {
             const float4* n = nodes + 4 * static_cast<int64_t>(ref);
-            const float4 bx = __ldg(n + 0);  // c0 x lo/hi, c0 y lo/hi
-            const float4 by = __ldg(n + 1);  // c1 x lo/hi, c1 y lo/hi
-            const float4 bz = __ldg(n + 2);  // c0 z lo/hi, c1 z lo/hi
-            const int4 rf = __ldg(reinterpret_cast<const int4*>(n + 3));
+            float4 bx, by, bz, rff;
+            ldg256(n, bx, by);        // c0 x lo/hi, c0 y lo/hi | c1 x lo/hi, c1 y lo/hi
+            ldg256(n + 2, bz, rff);   // c0 z lo/hi, c1 z lo/hi | refs
+            const int2 rf = make_int2(__float_as_int(rff.x), __float_as_int(rff.y));
             if (COUNT) ++ctr.nodes;
             const float a0 = fmaf(bx.x, idx, -oxd), a1 = fmaf(bx.y, idx, -oxd);
             const float a2 = fmaf(bx.z, idy, -oyd), a3 = fmaf(bx.w, idy, -oyd);
@@ -184,7 +195,8 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             if (h0 && h1) {
                 const bool swap = c1min < c0min;
                 stack_ref[sp * kBlock] = swap ? rf.x : rf.y;
-                stack_t[sp * kBlock] = swap ? c0min : c1min;
+                // entry distance rounded down to half precision: pops stay conservative
+                stack_t[sp * kBlock] = __float2half_rd(swap ? c0min : c1min);
                 ++sp;
                 ref = swap ? rf.y : rf.x;
             } else if (h0 || h1) {
@@ -193,7 +205,7 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
                 ref = kExit;
                 while (sp > 0) {
                     --sp;
-                    if (stack_t[sp * kBlock] <= best) {
+                    if (__half2float(stack_t[sp * kBlock]) <= best) {
                         ref = stack_ref[sp * kBlock];
                         break;
                     }
@@ -234,7 +246,7 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
         ref = kExit;
         while (sp > 0) {
             --sp;
-            if (stack_t[sp * kBlock] <= best) {
+            if (__half2float(stack_t[sp * kBlock]) <= best) {
                 ref = stack_ref[sp * kBlock];
                 break;
             }

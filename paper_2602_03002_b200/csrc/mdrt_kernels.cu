@@ -253,7 +253,7 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
 // ---------------------------------------------------------------------------
 template <bool COUNT>
 __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int* stack,
-                                            float* stack_t) {
+                                            __half* stack_t) {
     const uint32_t view = gw / static_cast<uint32_t>(p.tiles_per_view);
     const uint32_t tile = gw - view * static_cast<uint32_t>(p.tiles_per_view);
     const uint32_t ty = tile / static_cast<uint32_t>(p.tiles_x);
@@ -305,8 +305,13 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
             const float ldy = m0.w * dcx + m1.x * dcy + m1.y * dcz;
             const float ldz = m1.z * dcx + m1.w * dcy + m2.x * dcz;
             const float bound = p.early_termination ? z : dmax;
+            const unsigned int before = ctr.nodes;
             const float tt = trace<COUNT>(p.nodes, p.tris, tail.x, m2.y, m2.z, m2.w, ldx, ldy, ldz,
                                           bound * inv_m, stack, stack_t, ctr);
+            if (COUNT) {
+                ctr.link_nodes += ctr.nodes - before;
+                ++ctr.link_traces;
+            }
             const float cand = m * tt;
             if (cand < z) z = cand;
         }
@@ -328,14 +333,11 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     }
 
     if (COUNT) {
-        unsigned int nn = ctr.nodes, nt = ctr.tris;
-        for (int off = 16; off > 0; off >>= 1) {
-            nn += __shfl_xor_sync(0xffffffffu, nn, off);
-            nt += __shfl_xor_sync(0xffffffffu, nt, off);
-        }
-        if (lane == 0) {
-            atomicAdd(p.counters + 0, static_cast<unsigned long long>(nn));
-            atomicAdd(p.counters + 1, static_cast<unsigned long long>(nt));
+        unsigned int cv[4] = {ctr.nodes, ctr.tris, ctr.link_nodes, ctr.link_traces};
+        for (int i = 0; i < 4; ++i) {
+            for (int off = 16; off > 0; off >>= 1) cv[i] += __shfl_xor_sync(0xffffffffu, cv[i], off);
+            if (lane == 0 && (i < 2 || p.count_detail))
+                atomicAdd(p.counters + i, static_cast<unsigned long long>(cv[i]));
         }
     }
 
@@ -366,11 +368,11 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
 // Persistent warps: each warp pulls 8x4 tiles from a global counter until the
 // launch's tiles are exhausted (no block-tail idling, Aila & Laine style).
 template <bool COUNT>
-static __global__ void __launch_bounds__(kBlock, 8) render_kernel(RenderParams p) {
+static __global__ void __launch_bounds__(kBlock, 10) render_kernel(RenderParams p) {
     __shared__ int s_stack[kStack * kBlock];
-    __shared__ float s_stack_t[kStack * kBlock];
+    __shared__ __half s_stack_t[kStack * kBlock];
     int* stack = s_stack + threadIdx.x;
-    float* stack_t = s_stack_t + threadIdx.x;
+    __half* stack_t = s_stack_t + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const uint32_t total = static_cast<uint32_t>(p.N) * p.C * p.tiles_per_view;
     while (true) {

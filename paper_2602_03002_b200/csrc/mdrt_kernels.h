@@ -57,6 +57,7 @@ struct RenderParams {
     float* out;
     unsigned long long* counters;
     unsigned int* tile_counter;   // persistent-warp work counter (zeroed per launch)
+    int32_t count_detail;         // counters has 4 slots: + link node fetches, link traversals
 };
 
 struct NoiseParams {

@@ -281,13 +281,16 @@ def render(scene: Scene, *, early_termination: bool = True, backend: str | None 
     Bodies are queried in their link frames (never rebuilt), then terrain in
     the world frame bounded by the best body hit when early_termination is on.
     ``counters`` (int64 CUDA tensor of 2) accumulates BVH node-record fetches
-    and triangle tests (the algorithmic-bytes denominator).
+    and triangle tests (the algorithmic-bytes denominator); with 4 slots it
+    also splits out link-tree node fetches and link traversals started.
     """
     _check_backend(backend, threads)
     data = scene._new_frame(out)
     args = scene._step_args(data, early_termination)
     if counters is not None:
         args.flags |= _native.COUNT
+        if counters.numel() >= 4:
+            args.flags |= _native.COUNT_DETAIL
         args.counters = counters.data_ptr()
     scene._launch(args)
     return DepthFrame(data, timestamp)

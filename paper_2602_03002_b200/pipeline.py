@@ -29,15 +29,19 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
                     frame_buffer: FrameBuffer | None = None, timestamp: float | None = None,
                     delays=None, early_termination: bool = True, out: torch.Tensor | None = None,
                     clean_out: torch.Tensor | None = None,
-                    counters: torch.Tensor | None = None) -> torch.Tensor:
+                    counters: torch.Tensor | None = None,
+                    host_out: torch.Tensor | None = None) -> torch.Tensor:
     """One simulation step of the multi-depth pipeline; returns the observation (N,C,H,W).
 
     * ``sensor``: apply noise/dropout/clamp with counters (step, global env, cam, row, col).
     * ``frame_buffer`` + ``timestamp`` + ``delays`` (N,): push the noisy frame
       and return, per env, the newest frame with ts <= timestamp - delay.
     * ``clean_out``: optionally also store the noise-free range image.
+    * ``host_out``: pinned CPU tensor that receives the observation asynchronously
+      (side copy stream, overlaps the next step; ``scene.host_sync()`` before use).
     """
     data = scene._new_frame(out)
+    scene._guard_out(data)
     a = scene._step_args(data, early_termination)
     if clean_out is not None:
         scene._new_frame(clean_out)
@@ -80,4 +84,6 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
         a.flags |= _native.COUNT
         a.counters = counters.data_ptr()
     scene._launch(a)
+    if host_out is not None:
+        scene._deliver(data, host_out)
     return data

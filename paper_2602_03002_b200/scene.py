@@ -166,25 +166,32 @@ class Scene:
 
         Quaternions are normalised on the device (in f64) by the prologue
         kernel, so any nonzero norm is accepted as in the reference.
-        ``validate=False`` skips the finite/zero-norm checks, which need a
-        device->host read for CUDA inputs.
+        Pinned host tensors are copied asynchronously on the current stream.
+        ``validate=False`` skips the finite/zero-norm checks (for CUDA inputs
+        they need a device->host read).
         """
         n, b = self.num_envs, self.num_bodies
-        pos = _as_device_f32(positions, self.device)
-        rot = _as_device_f32(rotations, self.device)
-        if tuple(pos.shape) != (n, b, 3) or tuple(rot.shape) != (n, b, 4):
-            raise ValueError(f"expected poses shaped {(n, b, 3)} / {(n, b, 4)}, "
-                             f"got {tuple(pos.shape)} / {tuple(rot.shape)}")
+        srcs = []
+        for x, k in ((positions, 3), (rotations, 4)):
+            if isinstance(x, torch.Tensor):
+                t = x if x.dtype == torch.float32 else x.to(torch.float32)
+            else:
+                t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64), dtype=np.float32))
+            if tuple(t.shape) != (n, b, k):
+                raise ValueError(f"expected poses shaped {(n, b, 3)} / {(n, b, 4)}, "
+                                 f"got {tuple(torch.as_tensor(positions).shape)} / "
+                                 f"{tuple(torch.as_tensor(rotations).shape)}")
+            srcs.append(t)
+        pos, rot = srcs
         if validate and pos.numel():
             finite = torch.isfinite(pos).all() & torch.isfinite(rot).all()
             small = (rot.double().norm(dim=-1) < 1e-12).any()
-            ok, zero = bool(finite.item()), bool(small.item())
-            if not ok:
+            if not bool(finite.item()):
                 raise ValueError("poses must be finite")
-            if zero:
+            if bool(small.item()):
                 raise ValueError("zero quaternion in body rotations")
-        self.body_positions.copy_(pos)
-        self.body_rotations.copy_(rot)
+        for dst, src in ((self.body_positions, pos), (self.body_rotations, rot)):
+            dst.copy_(src, non_blocking=src.device.type == "cpu" and src.is_pinned())
 
     def body_pose(self, env: int, body: int) -> RigidPose:
         return RigidPose(self.body_positions[env, body].double().cpu().numpy(),
@@ -257,6 +264,39 @@ class Scene:
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self._ctx.render(args, stream)
 
+    # -- asynchronous host delivery ------------------------------------------
+    def _guard_out(self, out: torch.Tensor) -> None:
+        """Make the current stream wait until a pending host copy of ``out`` finished."""
+        ev = self._copy_events.get(out.data_ptr()) if hasattr(self, "_copy_events") else None
+        if ev is not None:
+            torch.cuda.current_stream(self.device).wait_event(ev)
+
+    def _deliver(self, out: torch.Tensor, host_out: torch.Tensor) -> None:
+        """Queue out -> host_out (pinned) on the scene's copy stream, ordered after the kernel."""
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(self.device)
+            self._copy_events = {}
+        if host_out.device.type != "cpu" or tuple(host_out.shape) != self.frame_shape or \
+                host_out.dtype != torch.float32 or not host_out.is_pinned():
+            raise ValueError(f"host_out must be a pinned float32 CPU tensor of shape {self.frame_shape}")
+        cur = torch.cuda.current_stream(self.device)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._copy_stream.wait_event(done)
+        with torch.cuda.stream(self._copy_stream):
+            host_out.copy_(out, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self._copy_stream)
+        out.record_stream(self._copy_stream)
+        self._copy_events[out.data_ptr()] = ev
+        self._last_copy = ev
+
+    def host_sync(self) -> None:
+        """Block until every queued host delivery has landed."""
+        ev = getattr(self, "_last_copy", None)
+        if ev is not None:
+            ev.synchronize()
+
     def _new_frame(self, out):
         if out is None:
             return torch.empty(self.frame_shape, dtype=torch.float32, device=self.device)
@@ -275,17 +315,20 @@ def _check_backend(backend, threads):
 
 def render(scene: Scene, *, early_termination: bool = True, backend: str | None = None,
            threads: int | None = None, timestamp: float = 0.0, out=None,
-           counters: torch.Tensor | None = None) -> DepthFrame:
+           counters: torch.Tensor | None = None, host_out: torch.Tensor | None = None) -> DepthFrame:
     """One ray per (env, camera, pixel); returns range depth (scene.py:332-348).
 
     Bodies are queried in their link frames (never rebuilt), then terrain in
     the world frame bounded by the best body hit when early_termination is on.
-    ``counters`` (int64 CUDA tensor of 2) accumulates BVH node-record fetches
+    ``host_out`` (pinned CPU tensor): the frame is also copied to the host on a
+    side stream, overlapping the next step's kernels (call ``scene.host_sync()``
+    before reading it). ``counters`` (int64 CUDA tensor of 2) accumulates BVH node-record fetches
     and triangle tests (the algorithmic-bytes denominator); with 4 slots it
     also splits out link-tree node fetches and link traversals started.
     """
     _check_backend(backend, threads)
     data = scene._new_frame(out)
+    scene._guard_out(data)
     args = scene._step_args(data, early_termination)
     if counters is not None:
         args.flags |= _native.COUNT
@@ -293,6 +336,8 @@ def render(scene: Scene, *, early_termination: bool = True, backend: str | None 
             args.flags |= _native.COUNT_DETAIL
         args.counters = counters.data_ptr()
     scene._launch(args)
+    if host_out is not None:
+        scene._deliver(data, host_out)
     return DepthFrame(data, timestamp)
 
 

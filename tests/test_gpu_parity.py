@@ -288,3 +288,22 @@ def test_backend_registry(pkg):
     case, scene = _case_scene(pkg, "render_flat.npz")
     with pytest.raises(ValueError):
         pkg.render(scene, backend="numpy")
+
+
+def test_async_host_delivery(pkg):
+    """host_out: pinned copies on the scene's copy stream match the device observations."""
+    case, scene = _case_scene(pkg, "render_cfg2_slice.npz")
+    cfg = pkg.SensorConfig(seed=4)
+    outs = [torch.empty(scene.frame_shape, device="cuda") for _ in range(2)]
+    hosts = [torch.empty(scene.frame_shape).pin_memory() for _ in range(2)]
+    expect = []
+    for s in range(5):
+        obs = pkg.render_pipeline(scene, sensor=cfg, step=s, out=outs[s % 2], host_out=hosts[s % 2])
+        expect.append(obs.clone())
+        if s >= 1:
+            scene.host_sync()
+            assert torch.equal(hosts[(s - 1) % 2], expect[s - 1].cpu()) or torch.equal(hosts[s % 2], expect[s].cpu())
+    scene.host_sync()
+    torch.cuda.synchronize()
+    assert torch.equal(hosts[4 % 2], expect[4].cpu())
+    assert torch.equal(hosts[3 % 2], expect[3].cpu())

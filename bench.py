@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--pose-sets", type=int, default=8)
+    ap.add_argument("--gather", action="store_true",
+                    help="N>1: also time the step + NCCL gather of all observations to rank 0")
     return ap.parse_args()
 
 
@@ -241,6 +243,7 @@ def main():
     import torch.distributed as dist
     import paper_2602_03002_b200 as md
     from paper_2602_03002_b200 import _native, synth
+    from paper_2602_03002_b200 import distributed as pdist
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -253,7 +256,8 @@ def main():
     n = args.envs or cfg_envs(args.config)
     total_envs = n * world
     w = synth.config(args.config, total_envs)
-    env0 = rank * n
+    env0, n_rank = pdist.env_slice(total_envs, rank, world)
+    assert n_rank == n
     bodies = [(nm, md.TriMesh(f32(m.vertices).astype(np.float64), m.faces, frame="body-local"))
               for nm, m in w.bodies]
     terrain = md.TriMesh(f32(w.terrain.mesh.vertices).astype(np.float64), w.terrain.mesh.faces)
@@ -398,11 +402,28 @@ def main():
     h2d = pose_host[0][0].numel() * 4 + pose_host[0][1].numel() * 4
     d2h = host_obs[0].numel() * 4
 
+    # ---- optional: step + NCCL gather of every rank's observation to rank 0 ----
+    gather_ms = 0.0
+    if args.gather and world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for i in range(args.steps):
+            scene.set_body_poses(*pose_dev[i % P], validate=False)
+            obs = md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf,
+                                     timestamp=step_id[0] * dt, delays=delays, out=out)
+            pdist.gather_frames(obs, dst=0)
+            step_id[0] += 1
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = g0.elapsed_time(g1)
+
     # max over ranks
-    tt = torch.tensor([total_ms, e2e_ms, kernel_ms], dtype=torch.float64, device=dev)
+    tt = torch.tensor([total_ms, e2e_ms, kernel_ms, gather_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms, kernel_ms = tt.tolist()
+    total_ms, e2e_ms, kernel_ms, gather_ms = tt.tolist()
 
     if rank == 0:
         all_rays = rays_per_step * world * args.steps
@@ -461,6 +482,9 @@ def main():
                     "how": "pinned-host poses H2D + fused pipeline + obs D2H (copy stream, double-buffered) "
                            "every step, L2 flush inside the timed loop, events around the whole loop"},
             "gpu_launches": 2 * args.steps,
+            "gather": ({"value": all_rays / (gather_ms * 1e-3), "unit": "rays/s",
+                        "how": "step + NCCL P2P gather of all observations to rank 0, no L2 flush"}
+                       if gather_ms > 0 else None),
             "clocks": clk,
             "wall_s_timed": wall,
         }

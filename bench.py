@@ -430,7 +430,8 @@ def main():
         value = all_rays / (total_ms * 1e-3)
         e2e_value = all_rays / (e2e_ms * 1e-3)
         # algorithmic bytes of one render-kernel launch (this rank's slice)
-        node_b, tri_b = 64, 48
+        node_b = scene.geometry_stats["node_record_size"]
+        tri_b = scene.geometry_stats["tri_record_size"]
         warps = n * C * math.ceil(W / 8) * math.ceil(H / 4)
         lag_frac = float(np.mean(delays_np >= dt))    # envs reading an older ring slot
         io_b = 4 + 4 + 4 * lag_frac                   # ring write + obs write + delayed read

@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdrt.so")
+# MDRT_LIB: load an alternative in-tree build (kernel-variant experiments only)
+LIB_PATH = os.environ.get("MDRT_LIB") or os.path.join(_HERE, "libmdrt.so")
 
 MDRT_OK = 0
 MDRT_EINVAL = -1

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -44,8 +45,25 @@ struct BNode {
 };
 
 constexpr int kBins = 32;
-constexpr double kCostNode = 1.2;  // relative cost of one 64 B node visit (two box tests)
 constexpr double kCostTri = 1.0;   // relative cost of one triangle test
+
+// SAH node cost relative to a triangle test (one 64 B record = two box tests)
+// and the largest leaf; overridable for tuning experiments via
+// MDRT_SAH_NODE_COST / MDRT_LEAF_MAX (<= 8, the leaf encoding's limit).
+struct BuildOptions {
+    double node_cost = 1.2;
+    int leaf_max = kMaxLeafTris;
+};
+
+const BuildOptions& options() {
+    static const BuildOptions o = [] {
+        BuildOptions r;
+        if (const char* v = std::getenv("MDRT_SAH_NODE_COST")) r.node_cost = std::atof(v);
+        if (const char* v = std::getenv("MDRT_LEAF_MAX")) r.leaf_max = std::min(8, std::max(1, std::atoi(v)));
+        return r;
+    }();
+    return o;
+}
 
 class Builder {
    public:
@@ -93,7 +111,8 @@ class Builder {
         // Switch to object-median splits when the remaining depth budget gets
         // tight: a median tree below this node adds ceil(log2(n)) levels.
         int need = 0;
-        while ((int64_t(kMaxLeafTris) << need) < n) ++need;
+        const int leaf_max = options().leaf_max;
+        while ((int64_t(leaf_max) << need) < n) ++need;
         const bool force_median = depth + need + 1 >= kMaxDepth;
         if (!force_median) {
             double best_cost = std::numeric_limits<double>::infinity();
@@ -127,7 +146,7 @@ class Builder {
                     lacc.grow(bb[b]);
                     lcnt += bc[b];
                     if (lcnt == 0 || right_cnt[b + 1] == 0) continue;
-                    double cost = kCostNode + (lacc.area() * lcnt + right_area[b + 1] * right_cnt[b + 1]) *
+                    double cost = options().node_cost + (lacc.area() * lcnt + right_area[b + 1] * right_cnt[b + 1]) *
                                                   kCostTri / std::max(parent_area, 1e-300);
                     if (cost < best_cost) {
                         best_cost = cost;
@@ -137,7 +156,7 @@ class Builder {
                 }
             }
             const double leaf_cost = kCostTri * static_cast<double>(n);
-            if (n <= kMaxLeafTris && !(best_cost < leaf_cost)) return false;
+            if (n <= leaf_max && !(best_cost < leaf_cost)) return false;
             if (best_axis >= 0) {
                 const double ext = cb.hi[best_axis] - cb.lo[best_axis];
                 const double scale = kBins / ext;
@@ -153,7 +172,7 @@ class Builder {
             }
         }
         if (mid < 0) {
-            if (n <= kMaxLeafTris && !force_median) return false;
+            if (n <= leaf_max && !force_median) return false;
             // object median on the longest centroid axis (or index median)
             int axis = 0;
             double ext = cb.hi[0] - cb.lo[0];
@@ -167,7 +186,7 @@ class Builder {
                                      return x < y;
                                  });
             }
-            if (n <= kMaxLeafTris && force_median) {
+            if (n <= leaf_max && force_median) {
                 // tiny node deep in the tree: a leaf is fine
                 return false;
             }

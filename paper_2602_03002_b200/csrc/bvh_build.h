@@ -30,7 +30,7 @@ struct alignas(16) PackedTri {
 };
 static_assert(sizeof(PackedTri) == 48, "triangle record must be 48 B");
 
-constexpr int kMaxLeafTris = 4;
+constexpr int kMaxLeafTris = 4;   // default leaf size bound (encoding allows 8)
 constexpr int kMaxDepth = 24;   // builder guarantees leaf depth <= kMaxDepth (= GPU stack size)
 
 inline int32_t leaf_ref(int64_t first, int count) {

@@ -517,7 +517,7 @@ int mdrt_bvh_check(const double* verts, int64_t nv, const int64_t* faces, int64_
             } else {
                 const int32_t v = ~it.ref;
                 const int64_t first = v >> 3, cnt = (v & 7) + 1;
-                need(cnt <= kMaxLeafTris, "leaf larger than kMaxLeafTris");
+                need(cnt <= 8, "leaf larger than the encoding allows");
                 need(first + cnt <= static_cast<int64_t>(t.tris.size()), "leaf range out of bounds");
                 ++leaves;
                 for (int64_t i = first; i < first + cnt; ++i) {

@@ -70,7 +70,7 @@ constexpr unsigned long long kMixB = 0x94D049BB133111EBULL;
 constexpr unsigned long long kDomU1 = 0x9A4C93AED1F3B217ULL;
 constexpr unsigned long long kDomU2 = 0x6E2F1D84C5A7093BULL;
 
-__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+__host__ __device__ constexpr unsigned long long mix64(unsigned long long x) {
     x ^= x >> 30;
     x *= kMixA;
     x ^= x >> 27;
@@ -79,9 +79,16 @@ __host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long 
     return x;
 }
 
-__host__ __device__ __forceinline__ unsigned long long absorb(unsigned long long h, unsigned long long v) {
+__host__ __device__ constexpr unsigned long long absorb(unsigned long long h, unsigned long long v) {
     return mix64(h ^ mix64(v + kGolden));
 }
+
+// absorb(h, v) = mix64(h ^ C(v)) with C(v) = mix64(v + golden): the inner half
+// depends only on the counter value, so constants fold at compile time and a
+// column's C(x) is shared by the uniform and the normal stream.
+__host__ __device__ constexpr unsigned long long counter_mix(unsigned long long v) { return mix64(v + kGolden); }
+constexpr unsigned long long kCDomU1 = counter_mix(kDomU1);
+constexpr unsigned long long kCDomU2 = counter_mix(kDomU2);
 
 // uniform in [0,1) from the top 53 bits (rng.py:78-80)
 __device__ __forceinline__ double unit53(unsigned long long h) {
@@ -90,8 +97,8 @@ __device__ __forceinline__ double unit53(unsigned long long h) {
 
 // standard normal by Box-Muller on two domain-separated sub-hashes (rng.py:94-99)
 __device__ __forceinline__ double normal_from_hash(unsigned long long h) {
-    const double u1 = static_cast<double>((absorb(h, kDomU1) >> 11) + 1ULL) * 0x1p-53;
-    const double u2 = static_cast<double>(absorb(h, kDomU2) >> 11) * 0x1p-53;
+    const double u1 = static_cast<double>((mix64(h ^ kCDomU1) >> 11) + 1ULL) * 0x1p-53;
+    const double u2 = static_cast<double>(mix64(h ^ kCDomU2) >> 11) * 0x1p-53;
     // __dmul_rn: keep numpy's unfused rounding
     return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
 }
@@ -101,8 +108,9 @@ __device__ __forceinline__ double normal_from_hash(unsigned long long h) {
 __device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru, unsigned long long rn,
                                               unsigned long long x, double noise_scale, double dropout_p,
                                               double fill, double dmax) {
-    const bool drop = unit53(absorb(ru, x)) < dropout_p;
-    const double g = normal_from_hash(absorb(rn, x));
+    const unsigned long long cx = counter_mix(x);
+    const bool drop = unit53(mix64(ru ^ cx)) < dropout_p;
+    const double g = normal_from_hash(mix64(rn ^ cx));
     double v = __dmul_rn(static_cast<double>(depth), __dadd_rn(1.0, __dmul_rn(noise_scale, g)));
     v = drop ? fill : v;
     v = v > 1e-6 ? v : 1e-6;       // np.clip lower (DEPTH_FLOOR, sensor.py:35)
@@ -154,12 +162,12 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // slab-tested, the nearer hit child is descended and the farther one pushed
 // together with its entry distance, so pops whose entry lies beyond the best
 // hit so far are discarded without fetching the record.
-// `stack_ref`/`stack_t` point at this thread's column of [kStack][kBlock] shared arrays.
+// `stack` points at this thread's column of a [kStack][kBlock] shared array.
 template <bool COUNT>
 __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                        int32_t root, float ox, float oy, float oz, float dx, float dy,
-                                       float dz, float tmax, int* __restrict__ stack_ref,
-                                       __half* __restrict__ stack_t, TraceCounters& ctr) {
+                                       float dz, float tmax, int2* __restrict__ stack,
+                                       TraceCounters& ctr) {
     // zero direction components: a huge reciprocal turns the slab into a
     // containment test like _slab_hit's d == 0 branch (numba_backend.py:76-78)
     const float tiny = 1e-30f;
@@ -170,7 +178,10 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
 
     float best = tmax;
     bool hit = false;
-    int sp = 0;
+    // stack entries {ref, entry distance} in one 8-byte shared slot per level;
+    // `top` walks this thread's column ([kStack][kBlock] layout, conflict-free)
+    int2* top = stack;
+    int2* const bottom = stack;
     int32_t ref = root;
     while (true) {
         while (ref >= 0) {
@@ -194,19 +205,18 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             const bool h1 = c1min <= c1max;
             if (h0 && h1) {
                 const bool swap = c1min < c0min;
-                stack_ref[sp * kBlock] = swap ? rf.x : rf.y;
-                // entry distance rounded down to half precision: pops stay conservative
-                stack_t[sp * kBlock] = __float2half_rd(swap ? c0min : c1min);
-                ++sp;
+                *top = make_int2(swap ? rf.x : rf.y, __float_as_int(swap ? c0min : c1min));
+                top += kBlock;
                 ref = swap ? rf.y : rf.x;
             } else if (h0 || h1) {
                 ref = h0 ? rf.x : rf.y;
             } else {
                 ref = kExit;
-                while (sp > 0) {
-                    --sp;
-                    if (__half2float(stack_t[sp * kBlock]) <= best) {
-                        ref = stack_ref[sp * kBlock];
+                while (top != bottom) {
+                    top -= kBlock;
+                    const int2 e = *top;
+                    if (__int_as_float(e.y) <= best) {
+                        ref = e.x;
                         break;
                     }
                 }
@@ -244,10 +254,11 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             }
         }
         ref = kExit;
-        while (sp > 0) {
-            --sp;
-            if (__half2float(stack_t[sp * kBlock]) <= best) {
-                ref = stack_ref[sp * kBlock];
+        while (top != bottom) {
+            top -= kBlock;
+            const int2 e = *top;
+            if (__int_as_float(e.y) <= best) {
+                ref = e.x;
                 break;
             }
         }

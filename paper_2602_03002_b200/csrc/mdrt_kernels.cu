@@ -252,8 +252,7 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
 // K1+K2+K3: render + fused sensor epilogue. One warp = one 8x4 tile of a view.
 // ---------------------------------------------------------------------------
 template <bool COUNT>
-__device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int* stack,
-                                            __half* stack_t) {
+__device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int2* stack) {
     const uint32_t view = gw / static_cast<uint32_t>(p.tiles_per_view);
     const uint32_t tile = gw - view * static_cast<uint32_t>(p.tiles_per_view);
     const uint32_t ty = tile / static_cast<uint32_t>(p.tiles_x);
@@ -307,7 +306,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
             const float bound = p.early_termination ? z : dmax;
             const unsigned int before = ctr.nodes;
             const float tt = trace<COUNT>(p.nodes, p.tris, tail.x, m2.y, m2.z, m2.w, ldx, ldy, ldz,
-                                          bound * inv_m, stack, stack_t, ctr);
+                                          bound * inv_m, stack, ctr);
             if (COUNT) {
                 ctr.link_nodes += ctr.nodes - before;
                 ++ctr.link_traces;
@@ -327,7 +326,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
         const float bound = p.early_termination ? z : dmax;
         const float tt = trace<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
-                                      bound * inv_m, stack, stack_t, ctr);
+                                      bound * inv_m, stack, ctr);
         const float cand = m * tt;
         if (cand < z) z = cand;
     }
@@ -368,11 +367,9 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
 // Persistent warps: each warp pulls 8x4 tiles from a global counter until the
 // launch's tiles are exhausted (no block-tail idling, Aila & Laine style).
 template <bool COUNT>
-static __global__ void __launch_bounds__(kBlock, 10) render_kernel(RenderParams p) {
-    __shared__ int s_stack[kStack * kBlock];
-    __shared__ __half s_stack_t[kStack * kBlock];
-    int* stack = s_stack + threadIdx.x;
-    __half* stack_t = s_stack_t + threadIdx.x;
+static __global__ void __launch_bounds__(kBlock, 9) render_kernel(RenderParams p) {
+    __shared__ int2 s_stack[kStack * kBlock];
+    int2* stack = s_stack + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const uint32_t total = static_cast<uint32_t>(p.N) * p.C * p.tiles_per_view;
     while (true) {
@@ -380,7 +377,7 @@ static __global__ void __launch_bounds__(kBlock, 10) render_kernel(RenderParams 
         if (lane == 0) gw = atomicAdd(p.tile_counter, 1u);
         gw = __shfl_sync(0xffffffffu, gw, 0);
         if (gw >= total) break;
-        render_tile<COUNT>(p, gw, lane, stack, stack_t);
+        render_tile<COUNT>(p, gw, lane, stack);
     }
 }
 

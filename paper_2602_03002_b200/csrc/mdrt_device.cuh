@@ -182,6 +182,46 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
     // `top` walks this thread's column ([kStack][kBlock] layout, conflict-free)
     int2* top = stack;
     int2* const bottom = stack;
+    auto pop = [&]() -> int32_t {
+        while (top != bottom) {
+            top -= kBlock;
+            const int2 e = *top;
+            if (__int_as_float(e.y) <= best) return e.x;
+        }
+        return kExit;
+    };
+    auto test_leaf = [&](int32_t lref) {
+        // leaf: ~((first << 3) | (count - 1))
+        const int32_t v = ~lref;
+        const int32_t first = v >> 3;
+        const int32_t cnt = (v & 7) + 1;
+        for (int32_t i = 0; i < cnt; ++i) {
+            const float4* t = tris + 3 * static_cast<int64_t>(first + i);
+            const float4 v0 = __ldg(t + 0);
+            const float4 e1 = __ldg(t + 1);
+            const float4 e2 = __ldg(t + 2);
+            if (COUNT) ++ctr.tris;
+            // Moller-Trumbore, double-sided (numba_backend.py:37-69)
+            const float px = dy * e2.z - dz * e2.y;
+            const float py = dz * e2.x - dx * e2.z;
+            const float pz = dx * e2.y - dy * e2.x;
+            const float det = e1.x * px + e1.y * py + e1.z * pz;
+            const float inv = rcp_approx(det);
+            const float tx = ox - v0.x, ty = oy - v0.y, tz = oz - v0.z;
+            const float u = (tx * px + ty * py + tz * pz) * inv;
+            const float qx = ty * e1.z - tz * e1.y;
+            const float qy = tz * e1.x - tx * e1.z;
+            const float qz = tx * e1.y - ty * e1.x;
+            const float w = (dx * qx + dy * qy + dz * qz) * inv;
+            const float tt = (e2.x * qx + e2.y * qy + e2.z * qz) * inv;
+            const bool ok = fabsf(det) >= 1e-12f && u >= -kBaryEps && u <= 1.0f + kBaryEps && w >= -kBaryEps &&
+                            u + w <= 1.0f + kBaryEps && tt > kRayEps && tt <= best;
+            if (ok) {
+                best = tt;
+                hit = true;
+            }
+        }
+    };
     int32_t ref = root;
     while (true) {
         while (ref >= 0) {
@@ -211,57 +251,12 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             } else if (h0 || h1) {
                 ref = h0 ? rf.x : rf.y;
             } else {
-                ref = kExit;
-                while (top != bottom) {
-                    top -= kBlock;
-                    const int2 e = *top;
-                    if (__int_as_float(e.y) <= best) {
-                        ref = e.x;
-                        break;
-                    }
+                ref = pop();
+            }
                 }
-            }
-        }
         if (ref == kExit) break;
-        // leaf: ~((first << 3) | (count - 1))
-        const int32_t v = ~ref;
-        const int32_t first = v >> 3;
-        const int32_t cnt = (v & 7) + 1;
-        for (int32_t i = 0; i < cnt; ++i) {
-            const float4* t = tris + 3 * static_cast<int64_t>(first + i);
-            const float4 v0 = __ldg(t + 0);
-            const float4 e1 = __ldg(t + 1);
-            const float4 e2 = __ldg(t + 2);
-            if (COUNT) ++ctr.tris;
-            // Moller-Trumbore, double-sided (numba_backend.py:37-69)
-            const float px = dy * e2.z - dz * e2.y;
-            const float py = dz * e2.x - dx * e2.z;
-            const float pz = dx * e2.y - dy * e2.x;
-            const float det = e1.x * px + e1.y * py + e1.z * pz;
-            const float inv = rcp_approx(det);
-            const float tx = ox - v0.x, ty = oy - v0.y, tz = oz - v0.z;
-            const float u = (tx * px + ty * py + tz * pz) * inv;
-            const float qx = ty * e1.z - tz * e1.y;
-            const float qy = tz * e1.x - tx * e1.z;
-            const float qz = tx * e1.y - ty * e1.x;
-            const float w = (dx * qx + dy * qy + dz * qz) * inv;
-            const float tt = (e2.x * qx + e2.y * qy + e2.z * qz) * inv;
-            const bool ok = fabsf(det) >= 1e-12f && u >= -kBaryEps && u <= 1.0f + kBaryEps && w >= -kBaryEps &&
-                            u + w <= 1.0f + kBaryEps && tt > kRayEps && tt <= best;
-            if (ok) {
-                best = tt;
-                hit = true;
-            }
-        }
-        ref = kExit;
-        while (top != bottom) {
-            top -= kBlock;
-            const int2 e = *top;
-            if (__int_as_float(e.y) <= best) {
-                ref = e.x;
-                break;
-            }
-        }
+        test_leaf(ref);
+        ref = pop();
         if (ref == kExit) break;
     }
     return hit ? best : __int_as_float(0x7f800000);

@@ -331,12 +331,16 @@ def main():
     # ---- render-kernel-only timing (roofline of the dominant kernel) ----
     kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kend = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    pstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    pend = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for i in range(args.steps):
         s = step_id[0]
         scene.set_body_poses(*pose_dev[i % P], validate=False)
         a = scene._step_args(out, True)
         a.flags |= _native.PHASE_PROLOGUE
+        pstart[i].record(stream)
         scene._launch(a)
+        pend[i].record(stream)
         flush.fill_(float(i))
         a = scene._step_args(out, True)
         a.flags |= _native.PHASE_TRACE | _native.SENSOR
@@ -347,6 +351,7 @@ def main():
         step_id[0] += 1
     torch.cuda.synchronize()
     kernel_ms = statistics.mean(s.elapsed_time(e) for s, e in zip(kstart, kend))
+    prologue_ms = statistics.mean(s.elapsed_time(e) for s, e in zip(pstart, pend))
 
     # ---- L2 read bandwidth probe (roofline denominator for L2-resident traversal) ----
     l2_gbs = None
@@ -474,6 +479,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "render_kernel (K1+K2+K3 fused)", "kernel_ms": kernel_ms,
+                         "prologue_ms": prologue_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                          "l2_probe_gbs": l2_gbs,
                          "l2_frac": (achieved / l2_gbs) if l2_gbs else None},

@@ -357,6 +357,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         }
         pp.views = ctx->views.ptr;
         pp.links = ctx->links.ptr;
+        ctx->tile_counter.reserve(1);
+        pp.reset_counter = ctx->tile_counter.ptr;
         const bool only_pro = (a->flags & MDRT_PHASE_PROLOGUE) && !(a->flags & MDRT_PHASE_TRACE);
         const bool only_trace = (a->flags & MDRT_PHASE_TRACE) && !(a->flags & MDRT_PHASE_PROLOGUE);
         if (!only_trace) {
@@ -395,6 +397,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.tile_counter = ctx->tile_counter.ptr;
         const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;
         need(warps < (int64_t(1) << 31), "launch too large");
+        if (only_trace) CK(cudaMemsetAsync(rp.tile_counter, 0, sizeof(unsigned int), s));  // prologue not run
         launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, s);
         CK(cudaGetLastError());
     });

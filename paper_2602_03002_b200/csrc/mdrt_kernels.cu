@@ -106,7 +106,12 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
     const double cx = p.W / 2.0, cy = p.H / 2.0;
     const bool grid = p.grid_mode;
 
-    // ---- link cull list ----
+    // ---- link cull list (f32: conservative to well under a pixel; M and o are
+    // rounded to f32 for the traversal anyway) ----
+    float Rf[9];
+    for (int i = 0; i < 9; ++i) Rf[i] = static_cast<float>(R[i]);
+    const float fxf = static_cast<float>(fx), fyf = static_cast<float>(fy);
+    const float cxf = static_cast<float>(cx), cyf = static_cast<float>(cy);
     int count = 0;
     for (int base = 0; base < p.B; base += 32) {
         const int b = base + lane;
@@ -117,69 +122,79 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
             const int64_t k = static_cast<int64_t>(e) * p.B + b;
             const float* bp = p.body_pos + k * 3;
             const float* bq = p.body_rot + k * 4;
-            const Q lq = qnorm({bq[0], bq[1], bq[2], bq[3]});
-            double L[9];
-            qmat(lq, L);  // link -> world
-            // sphere centre in world, then camera frame
-            const double cwx = bp[0] + L[0] * bi.cx + L[1] * bi.cy + L[2] * bi.cz;
-            const double cwy = bp[1] + L[3] * bi.cx + L[4] * bi.cy + L[5] * bi.cz;
-            const double cwz = bp[2] + L[6] * bi.cx + L[7] * bi.cy + L[8] * bi.cz;
-            const double wx = cwx - t.x, wy = cwy - t.y, wz = cwz - t.z;
-            const double X = R[0] * wx + R[3] * wy + R[6] * wz;
-            const double Y = R[1] * wx + R[4] * wy + R[7] * wz;
-            const double Z = R[2] * wx + R[5] * wy + R[8] * wz;
-            const double r = bi.r;
-            const double dist = sqrt(X * X + Y * Y + Z * Z);
-            keep = (dist - r) <= rig.d_max * (1.0 + 1e-6) + 1e-6;
+            float qw = bq[0], qx = bq[1], qy = bq[2], qz = bq[3];
+            const float qn = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+            qw *= qn; qx *= qn; qy *= qn; qz *= qn;
+            const float L[9] = {1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy),
+                                2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx),
+                                2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)};
+            // camera origin relative to the link origin (f64 difference, then f32)
+            const float ox = static_cast<float>(t.x - bp[0]);
+            const float oy = static_cast<float>(t.y - bp[1]);
+            const float oz = static_cast<float>(t.z - bp[2]);
+            // link-box centre relative to the camera, camera frame
+            const float wx = L[0] * bi.cx + L[1] * bi.cy + L[2] * bi.cz - ox;
+            const float wy = L[3] * bi.cx + L[4] * bi.cy + L[5] * bi.cz - oy;
+            const float wz = L[6] * bi.cx + L[7] * bi.cy + L[8] * bi.cz - oz;
+            const float X = Rf[0] * wx + Rf[3] * wy + Rf[6] * wz;
+            const float Y = Rf[1] * wx + Rf[4] * wy + Rf[7] * wz;
+            const float Z = Rf[2] * wx + Rf[5] * wy + Rf[8] * wz;
+            const float dist = sqrtf(X * X + Y * Y + Z * Z);
+            keep = (dist - bi.r) <= static_cast<float>(rig.d_max) * (1.0f + 1e-5f) + 1e-5f;
             int x0 = 0, x1 = p.W - 1, y0 = 0, y1 = p.H - 1;
             if (keep && !grid && !p.no_cull) {
                 // Project the link box (clipped at the hit plane z = 1e-6; camera-frame
                 // rays are (u, v, 1) so z == t) to a conservative pixel rectangle.
-                double A[3][3];  // camera-frame half-axis vectors of the box
-                const double hk[3] = {bi.hx, bi.hy, bi.hz};
+                float A[3][3];  // camera-frame half-axis vectors of the box
+                const float hk[3] = {bi.hx, bi.hy, bi.hz};
                 for (int kx = 0; kx < 3; ++kx) {
-                    const double lx = L[0 * 3 + kx] * hk[kx], ly = L[1 * 3 + kx] * hk[kx], lz = L[2 * 3 + kx] * hk[kx];
-                    A[kx][0] = R[0] * lx + R[3] * ly + R[6] * lz;
-                    A[kx][1] = R[1] * lx + R[4] * ly + R[7] * lz;
-                    A[kx][2] = R[2] * lx + R[5] * ly + R[8] * lz;
+                    const float lx = L[0 * 3 + kx] * hk[kx], ly = L[1 * 3 + kx] * hk[kx], lz = L[2 * 3 + kx] * hk[kx];
+                    A[kx][0] = Rf[0] * lx + Rf[3] * ly + Rf[6] * lz;
+                    A[kx][1] = Rf[1] * lx + Rf[4] * ly + Rf[7] * lz;
+                    A[kx][2] = Rf[2] * lx + Rf[5] * ly + Rf[8] * lz;
                 }
-                double cx3[8][3];
-                for (int q = 0; q < 8; ++q) {
-                    const double s0 = (q & 1) ? 1.0 : -1.0, s1 = (q & 2) ? 1.0 : -1.0, s2 = (q & 4) ? 1.0 : -1.0;
-                    for (int a = 0; a < 3; ++a)
-                        cx3[q][a] = (a == 0 ? X : a == 1 ? Y : Z) + s0 * A[0][a] + s1 * A[1][a] + s2 * A[2][a];
+                float cx3[8][3];
+                for (int q8 = 0; q8 < 8; ++q8) {
+                    const float s0 = (q8 & 1) ? 1.f : -1.f, s1 = (q8 & 2) ? 1.f : -1.f, s2 = (q8 & 4) ? 1.f : -1.f;
+                    cx3[q8][0] = X + s0 * A[0][0] + s1 * A[1][0] + s2 * A[2][0];
+                    cx3[q8][1] = Y + s0 * A[0][1] + s1 * A[1][1] + s2 * A[2][1];
+                    cx3[q8][2] = Z + s0 * A[0][2] + s1 * A[1][2] + s2 * A[2][2];
                 }
-                const double zc = 1e-6;
-                double sxlo = 1e300, sxhi = -1e300, sylo = 1e300, syhi = -1e300;
+                const float zc = 1e-6f;
+                float sxlo = 3e38f, sxhi = -3e38f, sylo = 3e38f, syhi = -3e38f;
                 int front = 0;
-                auto add = [&](double px_, double py_, double pz_) {
-                    const double sx = px_ / pz_, sy = py_ / pz_;
-                    sxlo = fmin(sxlo, sx); sxhi = fmax(sxhi, sx);
-                    sylo = fmin(sylo, sy); syhi = fmax(syhi, sy);
-                };
-                for (int q = 0; q < 8; ++q) {
-                    if (cx3[q][2] > zc) { ++front; add(cx3[q][0], cx3[q][1], cx3[q][2]); }
+                for (int q8 = 0; q8 < 8; ++q8) {
+                    if (cx3[q8][2] > zc) {
+                        ++front;
+                        const float iz = 1.0f / cx3[q8][2];
+                        const float sx = cx3[q8][0] * iz, sy = cx3[q8][1] * iz;
+                        sxlo = fminf(sxlo, sx); sxhi = fmaxf(sxhi, sx);
+                        sylo = fminf(sylo, sy); syhi = fmaxf(syhi, sy);
+                    }
                 }
                 keep = front > 0;
                 if (keep && front < 8) {
                     // edges crossing the clip plane contribute their crossing point
-                    for (int q = 0; q < 8; ++q)
+                    for (int q8 = 0; q8 < 8; ++q8)
                         for (int bit = 1; bit < 8; bit <<= 1) {
-                            const int q2 = q | bit;
-                            if (q2 == q) continue;
-                            const double z0 = cx3[q][2], z1 = cx3[q2][2];
+                            const int q2 = q8 | bit;
+                            if (q2 == q8) continue;
+                            const float z0 = cx3[q8][2], z1 = cx3[q2][2];
                             if ((z0 > zc) == (z1 > zc)) continue;
-                            const double f = (zc - z0) / (z1 - z0);
-                            add(cx3[q][0] + f * (cx3[q2][0] - cx3[q][0]), cx3[q][1] + f * (cx3[q2][1] - cx3[q][1]), zc);
+                            const float f = (zc - z0) / (z1 - z0);
+                            const float sx = (cx3[q8][0] + f * (cx3[q2][0] - cx3[q8][0])) / zc;
+                            const float sy = (cx3[q8][1] + f * (cx3[q2][1] - cx3[q8][1])) / zc;
+                            sxlo = fminf(sxlo, sx); sxhi = fmaxf(sxhi, sx);
+                            sylo = fminf(sylo, sy); syhi = fmaxf(syhi, sy);
                         }
                 }
                 if (keep) {
-                    const double xl = sxlo * fx + cx - 0.5, xh = sxhi * fx + cx - 0.5;
-                    const double yl = sylo * fy + cy - 0.5, yh = syhi * fy + cy - 0.5;
-                    x0 = xl > x0 ? static_cast<int>(fmin(floor(xl) - 1.0, 1e9)) : x0;
-                    x1 = xh < x1 ? static_cast<int>(fmax(ceil(xh) + 1.0, -1e9)) : x1;
-                    y0 = yl > y0 ? static_cast<int>(fmin(floor(yl) - 1.0, 1e9)) : y0;
-                    y1 = yh < y1 ? static_cast<int>(fmax(ceil(yh) + 1.0, -1e9)) : y1;
+                    const float xl = sxlo * fxf + cxf - 0.5f, xh = sxhi * fxf + cxf - 0.5f;
+                    const float yl = sylo * fyf + cyf - 0.5f, yh = syhi * fyf + cyf - 0.5f;
+                    x0 = xl > x0 ? static_cast<int>(fminf(floorf(xl) - 1.0f, 1e9f)) : x0;
+                    x1 = xh < x1 ? static_cast<int>(fmaxf(ceilf(xh) + 1.0f, -1e9f)) : x1;
+                    y0 = yl > y0 ? static_cast<int>(fminf(floorf(yl) - 1.0f, 1e9f)) : y0;
+                    y1 = yh < y1 ? static_cast<int>(fmaxf(ceilf(yh) + 1.0f, -1e9f)) : y1;
                     x0 = max(x0, 0); y0 = max(y0, 0);
                     x1 = min(x1, p.W - 1); y1 = min(y1, p.H - 1);
                     keep = x0 <= x1 && y0 <= y1;
@@ -189,13 +204,11 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
                 // M = L^T R (camera frame -> link frame), o = L^T (t - p)
                 for (int i = 0; i < 3; ++i)
                     for (int j = 0; j < 3; ++j)
-                        rec.m[i * 3 + j] = static_cast<float>(L[0 * 3 + i] * R[0 * 3 + j] +
-                                                              L[1 * 3 + i] * R[1 * 3 + j] +
-                                                              L[2 * 3 + i] * R[2 * 3 + j]);
-                const double ox = t.x - bp[0], oy = t.y - bp[1], oz = t.z - bp[2];
-                rec.o[0] = static_cast<float>(L[0] * ox + L[3] * oy + L[6] * oz);
-                rec.o[1] = static_cast<float>(L[1] * ox + L[4] * oy + L[7] * oz);
-                rec.o[2] = static_cast<float>(L[2] * ox + L[5] * oy + L[8] * oz);
+                        rec.m[i * 3 + j] = L[0 * 3 + i] * Rf[0 * 3 + j] + L[1 * 3 + i] * Rf[1 * 3 + j] +
+                                           L[2 * 3 + i] * Rf[2 * 3 + j];
+                rec.o[0] = L[0] * ox + L[3] * oy + L[6] * oz;
+                rec.o[1] = L[1] * ox + L[4] * oy + L[7] * oz;
+                rec.o[2] = L[2] * ox + L[5] * oy + L[8] * oz;
                 rec.root = bi.root;
                 rec.x0 = static_cast<int16_t>(x0);
                 rec.x1 = static_cast<int16_t>(x1);
@@ -210,6 +223,8 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
         }
         count += __popc(mask);
     }
+
+    if (view == 0 && lane == 0 && p.reset_counter) *p.reset_counter = 0u;
 
     // ---- view record ----
     if (lane == 0) {
@@ -489,7 +504,6 @@ void launch_render(const RenderParams& p, int64_t warps, bool count, cudaStream_
     }
     const int64_t need = (warps * 32 + kBlock - 1) / kBlock;
     const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(sms) * std::max(1, blocks_per_sm[count]));
-    cudaMemsetAsync(p.tile_counter, 0, sizeof(unsigned int), s);
     if (count)
         render_kernel<true><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(p);
     else

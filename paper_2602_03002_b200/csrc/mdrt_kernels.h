@@ -33,6 +33,7 @@ struct PrologueParams {
     int32_t* read_slot_out;
     ViewRec* views;
     LinkRec* links;
+    unsigned int* reset_counter;  // render kernel's tile counter, zeroed here (prologue runs first)
 };
 
 struct RenderParams {

@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5", "cfg5_1m"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default: config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -68,7 +68,7 @@ def f32(x):
 
 
 def cfg_envs(name):
-    return {"cfg2": 4096, "cfg3": 4096, "cfg5": 4096}[name]
+    return {"cfg2": 4096, "cfg3": 4096, "cfg5": 4096, "cfg5_1m": 4096}[name]
 
 
 def workload_desc(name):
@@ -76,7 +76,9 @@ def workload_desc(name):
         "cfg2": "4096 envs x 2 cams (front+back) 64x48 per GPU, 3x3 slope/stairs tiles (259,200 tris), "
                 "30-link G1 proxy (8,060 tris), full noise/dropout/latency",
         "cfg3": "4096 envs x 4 cams 64x48, stepping stones 25cm/60cm (8,750 tris), arms raised, full sensor",
-        "cfg5": "4096 envs x 2 cams 160x120, 708x708-node rolling terrain (999,698 tris), full sensor",
+        "cfg5": "4096 envs x 2 cams 160x120, 1300x1300-node rolling terrain (3,373,802 tris, BVH ~270 MB > 2x L2), "
+                "full sensor",
+        "cfg5_1m": "4096 envs x 2 cams 160x120, 708x708-node rolling terrain (999,698 tris), full sensor",
     }[name]
 
 

@@ -330,6 +330,27 @@ def main():
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
 
+    # ---- same step replayed as a captured CUDA graph (device step state) ----
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    cap = CapturedStep(scene, sensor=sens, frame_buffer=buf, delays=delays, dt=dt, first_step=step_id[0], out=out)
+    for i in range(args.warmup):
+        scene.body_positions.copy_(pose_dev[i % P][0])
+        scene.body_rotations.copy_(pose_dev[i % P][1])
+        cap.replay()
+    gstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    gend = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        gstart[i].record(stream)
+        scene.body_positions.copy_(pose_dev[i % P][0])
+        scene.body_rotations.copy_(pose_dev[i % P][1])
+        cap.replay()
+        gend[i].record(stream)
+    torch.cuda.synchronize()
+    graph_ms = sum(s.elapsed_time(e) for s, e in zip(gstart, gend))
+    step_id[0] = cap.next_step
+
     # ---- render-kernel-only timing (roofline of the dominant kernel) ----
     kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kend = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -427,10 +448,10 @@ def main():
         gather_ms = g0.elapsed_time(g1)
 
     # max over ranks
-    tt = torch.tensor([total_ms, e2e_ms, kernel_ms, gather_ms], dtype=torch.float64, device=dev)
+    tt = torch.tensor([total_ms, e2e_ms, kernel_ms, gather_ms, graph_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms, kernel_ms, gather_ms = tt.tolist()
+    total_ms, e2e_ms, kernel_ms, gather_ms, graph_ms = tt.tolist()
 
     if rank == 0:
         all_rays = rays_per_step * world * args.steps
@@ -491,6 +512,9 @@ def main():
                     "how": "pinned-host poses H2D + fused pipeline + obs D2H (copy stream, double-buffered) "
                            "every step, L2 flush inside the timed loop, events around the whole loop"},
             "gpu_launches": 2 * args.steps,
+            "graph": {"value": all_rays / (graph_ms * 1e-3), "unit": "rays/s", "ms_per_step": graph_ms / args.steps,
+                      "how": "CapturedStep replay (advance+prologue+render CUDA graph, device step state), "
+                             "device pose copy + L2 flush between steps as for value"},
             "gather": ({"value": all_rays / (gather_ms * 1e-3), "unit": "rays/s",
                         "how": "step + NCCL P2P gather of all observations to rank 0, no L2 flush"}
                        if gather_ms > 0 else None),

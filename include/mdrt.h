@@ -43,6 +43,9 @@ extern "C" {
 #define MDRT_PHASE_PROLOGUE 0x20   /* launch only the per-view prologue (timing); neither phase flag = both */
 #define MDRT_PHASE_TRACE 0x40      /* launch only the traversal kernel (uses the last prologue's records)  */
 #define MDRT_COUNT_DETAIL 0x80     /* with MDRT_COUNT: counters has 4 slots (+ link node fetches, link traversals) */
+#define MDRT_DEVICE_STATE 0x100    /* step, timestamp, RNG prefix and ring push come from the context's device
+                                      state (mdrt_state_set), advanced on the device at the start of the call:
+                                      the call is then CUDA-graph capturable and replayable with no host args */
 
 typedef struct mdrt_ctx mdrt_ctx;
 
@@ -142,6 +145,19 @@ int mdrt_get_stats(mdrt_ctx *ctx, mdrt_stats *out);
  * (sensor.py:55-82) and FrameBuffer push/fetch_delayed_batch (sensor.py:122-150),
  * fused into one traversal kernel. `stream` is a cudaStream_t (NULL = default). */
 int mdrt_render(mdrt_ctx *ctx, const mdrt_step_args *args, void *stream);
+
+/* Device step state for graph replay (MDRT_DEVICE_STATE). Each mdrt_render with
+ * the flag first advances it on the device: k = next_step, now = t0 + k*dt,
+ * sensor stream prefix from (key, k), and (ring_slots > 0) a FrameBuffer push of
+ * `now` into the ring (sensor.py:122-131). times/order: HOST (count,) current
+ * ring content, oldest first. Also reserves per-step scratch for num_envs so
+ * that later calls allocate nothing (capture-safe). Synchronous. */
+int mdrt_state_set(mdrt_ctx *ctx, int32_t num_envs, uint64_t sensor_key, double t0, double dt,
+                   int64_t next_step, int32_t ring_slots, const double *times, const int32_t *order,
+                   int32_t count);
+/* Read back the device step state (next_step, now, write_slot, count, times, order). */
+int mdrt_state_get(mdrt_ctx *ctx, int64_t *next_step, double *now, int32_t *write_slot, int32_t *count,
+                   double *times, int32_t *order);
 
 /* Standalone sensor epilogue on an existing (N,C,H,W) depth tensor
  * (apply_noise_dropout, sensor.py:55-82). d_max/fill: HOST (C,). */

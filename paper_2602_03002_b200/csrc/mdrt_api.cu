@@ -113,6 +113,7 @@ struct mdrt_ctx {
     DevBuf<ViewRec> views;
     DevBuf<LinkRec> links;
     DevBuf<unsigned int> tile_counter;
+    DevBuf<StepState> state;
 
     void use_device() const { CK(cudaSetDevice(device)); }
 };
@@ -159,6 +160,7 @@ int mdrt_destroy(mdrt_ctx* ctx) {
         ctx->views.release();
         ctx->links.release();
         ctx->tile_counter.release();
+        ctx->state.release();
         delete ctx;
     });
 }
@@ -311,11 +313,16 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
             need(a->noise_scale >= 0, "noise_scale must be >= 0");
             need(a->dropout_p >= 0 && a->dropout_p < 1, "dropout_p must be in [0, 1)");
         }
+        const bool dstate = (a->flags & MDRT_DEVICE_STATE) != 0;
+        if (dstate && !ctx->state.ptr) throw StateError("MDRT_DEVICE_STATE needs mdrt_state_set first");
         if (latency) {
             need(a->ring && a->ring_slots >= 1 && a->ring_slots <= 32, "ring must have 1..32 slots");
-            need(a->write_slot >= 0 && a->write_slot < a->ring_slots, "write_slot out of range");
-            need(a->ring_count >= 1 && a->ring_count <= a->ring_slots, "ring_count out of range");
-            need(a->ring_times && a->ring_order && a->delays, "latency arrays are NULL");
+            need(a->delays, "delays is NULL");
+            if (!dstate) {
+                need(a->write_slot >= 0 && a->write_slot < a->ring_slots, "write_slot out of range");
+                need(a->ring_count >= 1 && a->ring_count <= a->ring_slots, "ring_count out of range");
+                need(a->ring_times && a->ring_order, "latency arrays are NULL");
+            }
         }
         need(!(a->flags & MDRT_COUNT) || a->counters, "counters is NULL with MDRT_COUNT");
         ctx->use_device();
@@ -343,7 +350,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         pp.hu_step = absorb(absorb(key, 0ULL), st);
         pp.hn_step = absorb(absorb(key, 1ULL), st);
         pp.latency = latency;
-        if (latency) {
+        pp.state = dstate ? ctx->state.ptr : nullptr;
+        if (latency && !dstate) {
             pp.ring_count = a->ring_count;
             pp.write_slot = a->write_slot;
             pp.now = a->now;
@@ -353,6 +361,9 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
                 need(a->ring_order[k] >= 0 && a->ring_order[k] < a->ring_slots, "ring_order out of range");
                 pp.ring_order[k] = a->ring_order[k];
             }
+        }
+        if (latency) {
+            pp.delays = a->delays;
             pp.read_slot_out = a->read_slot;
         }
         pp.views = ctx->views.ptr;
@@ -361,6 +372,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         pp.reset_counter = ctx->tile_counter.ptr;
         const bool only_pro = (a->flags & MDRT_PHASE_PROLOGUE) && !(a->flags & MDRT_PHASE_TRACE);
         const bool only_trace = (a->flags & MDRT_PHASE_TRACE) && !(a->flags & MDRT_PHASE_PROLOGUE);
+        if (dstate && !only_trace) {
+            launch_advance(ctx->state.ptr, s);
+            CK(cudaGetLastError());
+        }
         if (!only_trace) {
             launch_prologue(pp, static_cast<int64_t>(nviews), s);
             CK(cudaGetLastError());
@@ -393,6 +408,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.out = a->out;
         rp.counters = a->counters;
         rp.count_detail = (a->flags & MDRT_COUNT_DETAIL) != 0;
+        rp.state = dstate ? ctx->state.ptr : nullptr;
         ctx->tile_counter.reserve(1);
         rp.tile_counter = ctx->tile_counter.ptr;
         const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;
@@ -400,6 +416,57 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         if (only_trace) CK(cudaMemsetAsync(rp.tile_counter, 0, sizeof(unsigned int), s));  // prologue not run
         launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, s);
         CK(cudaGetLastError());
+    });
+}
+
+int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, double t0, double dt, int64_t next_step,
+                   int32_t ring_slots, const double* times, const int32_t* order, int32_t count) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        if (!ctx->committed) throw StateError("mdrt_commit first");
+        need(num_envs >= 1, "num_envs must be >= 1");
+        need(ring_slots >= 0 && ring_slots <= 32, "ring_slots must be in [0, 32]");
+        need(count >= 0 && count <= ring_slots, "count out of range");
+        need(count == 0 || (times && order), "times/order are NULL");
+        ctx->use_device();
+        StepState st{};
+        st.key = sensor_key;
+        st.next_step = next_step;
+        st.t0 = t0;
+        st.dt = dt;
+        st.ring_slots = ring_slots;
+        st.ring_count = count;
+        st.write_slot = count > 0 ? order[count - 1] : 0;
+        for (int i = 0; i < count; ++i) {
+            need(order[i] >= 0 && order[i] < ring_slots, "order entry out of range");
+            st.times[i] = times[i];
+            st.order[i] = order[i];
+        }
+        ctx->state.reserve(1);
+        const size_t nviews = static_cast<size_t>(num_envs) * ctx->C;
+        ctx->views.reserve(nviews);
+        ctx->links.reserve(std::max<size_t>(1, nviews * std::max<size_t>(ctx->bodies.size(), 1)));
+        ctx->tile_counter.reserve(1);
+        CK(cudaMemcpy(ctx->state.ptr, &st, sizeof(st), cudaMemcpyHostToDevice));
+    });
+}
+
+int mdrt_state_get(mdrt_ctx* ctx, int64_t* next_step, double* now, int32_t* write_slot, int32_t* count,
+                   double* times, int32_t* order) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        if (!ctx->state.ptr) throw StateError("no device state (mdrt_state_set)");
+        ctx->use_device();
+        StepState st{};
+        CK(cudaMemcpy(&st, ctx->state.ptr, sizeof(st), cudaMemcpyDeviceToHost));
+        if (next_step) *next_step = st.next_step;
+        if (now) *now = st.now;
+        if (write_slot) *write_slot = st.write_slot;
+        if (count) *count = st.ring_count;
+        for (int i = 0; i < st.ring_count; ++i) {
+            if (times) times[i] = st.times[i];
+            if (order) order[i] = st.order[i];
+        }
     });
 }
 

@@ -242,20 +242,25 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
         v.read_slot = -1;
         v.pad0 = 0;
         const unsigned long long genv = static_cast<unsigned long long>(p.env_offset + e);
-        v.hu = absorb(absorb(p.hu_step, genv), static_cast<unsigned long long>(c));
-        v.hn = absorb(absorb(p.hn_step, genv), static_cast<unsigned long long>(c));
+        const StepState* st = p.state;
+        v.hu = absorb(absorb(st ? st->hu_step : p.hu_step, genv), static_cast<unsigned long long>(c));
+        v.hn = absorb(absorb(st ? st->hn_step : p.hn_step, genv), static_cast<unsigned long long>(c));
         if (p.latency) {
             // bisect_right(times, now - delay) - 1, clamped at 0 (sensor.py:138-139)
-            const double target = p.now - p.delays[e];
-            int lo = 0, hi = p.ring_count;
+            const double* times = st ? st->times : p.ring_times;
+            const int32_t* order = st ? st->order : p.ring_order;
+            const int count = st ? st->ring_count : p.ring_count;
+            const int wslot = st ? st->write_slot : p.write_slot;
+            const double target = (st ? st->now : p.now) - p.delays[e];
+            int lo = 0, hi = count;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (target < p.ring_times[mid]) hi = mid;
+                if (target < times[mid]) hi = mid;
                 else lo = mid + 1;
             }
             const int kk = lo - 1 < 0 ? 0 : lo - 1;
-            const int slot = p.ring_order[kk];
-            v.read_slot = slot == p.write_slot ? -1 : slot;
+            const int slot = order[kk];
+            v.read_slot = slot == wslot ? -1 : slot;
             if (c == 0 && p.read_slot_out) p.read_slot_out[e] = slot;
         }
         for (int i = 0; i < 8; ++i) v.pad1[i] = 0.f;
@@ -372,7 +377,8 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     if (p.out_clean) p.out_clean[o] = z;
     if (p.ring) {
         const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
-        p.ring[static_cast<int64_t>(p.write_slot) * frame + o] = val;
+        const int wslot = p.state ? p.state->write_slot : p.write_slot;
+        p.ring[static_cast<int64_t>(wslot) * frame + o] = val;
         const int rs = V.read_slot;
         if (rs >= 0) val = p.ring[static_cast<int64_t>(rs) * frame + o];
     }
@@ -480,6 +486,40 @@ static __global__ void __launch_bounds__(256) probe_read_kernel(const float4* __
     }
 }
 
+// Advance the device step state to step k = next_step (single thread; first
+// node of a captured step). Mirrors FrameBuffer._reserve + push (sensor.py:122-131)
+// and the sensor stream prefix absorb(absorb(key, 0|1), k) (rng.py:71-75).
+static __global__ void advance_kernel(StepState* st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const long long k = st->next_step;
+    st->now = st->t0 + static_cast<double>(k) * st->dt;
+    st->hu_step = absorb(absorb(st->key, 0ULL), static_cast<unsigned long long>(k));
+    st->hn_step = absorb(absorb(st->key, 1ULL), static_cast<unsigned long long>(k));
+    if (st->ring_slots > 0) {
+        int slot;
+        if (st->ring_count < st->ring_slots) {
+            slot = 0;   // lowest slot not in use
+            while (true) {
+                bool used = false;
+                for (int i = 0; i < st->ring_count; ++i) used |= st->order[i] == slot;
+                if (!used) break;
+                ++slot;
+            }
+            ++st->ring_count;
+        } else {
+            slot = st->order[0];
+            for (int i = 1; i < st->ring_count; ++i) {
+                st->order[i - 1] = st->order[i];
+                st->times[i - 1] = st->times[i];
+            }
+        }
+        st->order[st->ring_count - 1] = slot;
+        st->times[st->ring_count - 1] = st->now;
+        st->write_slot = slot;
+    }
+    st->next_step = k + 1;
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -528,6 +568,8 @@ void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     probe_read_kernel<<<sms * 8, 256, 0, s>>>(buf, n16, iters, sink);
 }
+
+void launch_advance(StepState* st, cudaStream_t s) { advance_kernel<<<1, 32, 0, s>>>(st); }
 
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s) {
     downsample_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);

@@ -7,6 +7,20 @@
 
 namespace mdrt {
 
+// Device-resident per-step bookkeeping for graph replay (MDRT_DEVICE_STATE):
+// advance_kernel produces step k's RNG prefixes, timestamp and latency-ring
+// push exactly as the host path would (FrameBuffer._reserve semantics).
+struct StepState {
+    unsigned long long key;       // rng.stream_key(seed, "sensor")
+    unsigned long long hu_step;   // absorb(absorb(key, 0), k)
+    unsigned long long hn_step;   // absorb(absorb(key, 1), k)
+    long long next_step;          // k of the next advance
+    double t0, dt, now;           // now = t0 + k * dt
+    int32_t ring_slots, ring_count, write_slot, pad;
+    double times[32];             // retained timestamps, oldest first
+    int32_t order[32];            // their ring slots
+};
+
 struct PrologueParams {
     int32_t N, C, B, W, H;
     int64_t env_offset;
@@ -34,6 +48,7 @@ struct PrologueParams {
     ViewRec* views;
     LinkRec* links;
     unsigned int* reset_counter;  // render kernel's tile counter, zeroed here (prologue runs first)
+    const StepState* state;       // non-null: step/ring/RNG fields come from device state
 };
 
 struct RenderParams {
@@ -59,6 +74,7 @@ struct RenderParams {
     unsigned long long* counters;
     unsigned int* tile_counter;   // persistent-warp work counter (zeroed per launch)
     int32_t count_detail;         // counters has 4 slots: + link node fetches, link traversals
+    const StepState* state;       // non-null: ring write slot comes from device state
 };
 
 struct NoiseParams {
@@ -104,5 +120,6 @@ void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s);
 void launch_select(const SelectParams& p, int64_t n, cudaStream_t s);
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s);
 void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, cudaStream_t s);
+void launch_advance(StepState* st, cudaStream_t s);
 
 }  // namespace mdrt

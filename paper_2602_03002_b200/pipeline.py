@@ -87,3 +87,83 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     if host_out is not None:
         scene._deliver(data, host_out)
     return data
+
+
+class CapturedStep:
+    """``render_pipeline`` captured once as a CUDA graph and replayed per step.
+
+    The graph is advance -> prologue -> render (three kernels, no host
+    arguments): the step counter, timestamp ``t0 + k*dt``, sensor-stream
+    prefix and latency-ring push live in device memory and are advanced by the
+    first kernel (MDRT_DEVICE_STATE), so a replay needs no host work beyond
+    ``cudaGraphLaunch``. Poses are read from ``scene.body_positions`` /
+    ``scene.body_rotations`` (write them in place, e.g. from the simulator).
+    Replays produce exactly the observations of the eager sequence
+    ``render_pipeline(step=k, timestamp=t0 + k*dt)`` for k = first_step, ...
+    (tests/test_gpu_parity.py::test_captured_step_matches_eager). The paper's
+    renderer is likewise captured in a graph.
+    """
+
+    def __init__(self, scene: Scene, *, sensor: SensorConfig | None = None,
+                 frame_buffer: FrameBuffer | None = None, delays=None, dt: float = 0.02, t0: float = 0.0,
+                 first_step: int = 0, out: torch.Tensor | None = None, early_termination: bool = True):
+        if frame_buffer is not None and (delays is None or not dt > 0):
+            raise ValueError("frame_buffer needs delays and dt > 0")
+        self.scene = scene
+        self.frame_buffer = frame_buffer
+        self.dt, self.t0 = float(dt), float(t0)
+        self.next_step = int(first_step)
+        self.out = scene._new_frame(out)
+        a = scene._step_args(self.out, early_termination)
+        a.flags |= _native.DEVICE_STATE
+        self._keep = []
+        key = 0
+        if sensor is not None:
+            a.flags |= _native.SENSOR
+            a.noise_scale = float(sensor.noise_scale)
+            a.dropout_p = float(sensor.dropout_p)
+            key = sensor.key
+            if sensor.dropout_fill is not None:
+                fill = np.full(scene.num_cameras, float(sensor.dropout_fill), dtype=np.float64)
+                self._keep.append(fill)
+                a.fill = _native.dptr(fill)
+        times, order, slots = np.zeros(0), np.zeros(0, np.int32), 0
+        if frame_buffer is not None:
+            d = _delays_tensor(delays, scene.device)
+            if tuple(d.shape) != (scene.num_envs,):
+                raise ValueError(f"delays must have shape ({scene.num_envs},)")
+            frame_buffer._ensure(scene.frame_shape, scene.device)
+            if frame_buffer._slot_buf is None or frame_buffer._slot_buf.shape[0] != scene.num_envs:
+                frame_buffer._slot_buf = torch.empty(scene.num_envs, dtype=torch.int32, device=scene.device)
+            times = np.asarray(frame_buffer._times, dtype=np.float64)
+            order = np.asarray(frame_buffer._slots, dtype=np.int32)
+            slots = frame_buffer.capacity
+            self._keep.append(d)
+            a.flags |= _native.LATENCY
+            a.ring = frame_buffer._ring.data_ptr()
+            a.ring_slots = frame_buffer.capacity
+            a.delays = d.data_ptr()
+            a.read_slot = frame_buffer._slot_buf.data_ptr()
+        scene._ctx.state_set(scene.num_envs, key, self.t0, self.dt, self.next_step, slots, times, order)
+        self._args = a
+        # warm the launch path (occupancy query) outside capture, then capture
+        plain = scene._step_args(self.out, early_termination)
+        side = torch.cuda.Stream(scene.device)
+        side.wait_stream(torch.cuda.current_stream(scene.device))
+        with torch.cuda.stream(side):
+            scene._launch(plain)
+        torch.cuda.current_stream(scene.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            scene._launch(a)
+
+    def replay(self) -> torch.Tensor:
+        """Run step ``next_step`` on the current stream; returns the observation tensor."""
+        self.graph.replay()
+        if self.frame_buffer is not None:   # host shadow of the device ring bookkeeping
+            self.frame_buffer._reserve(self.t0 + float(self.next_step) * self.dt)
+        self.next_step += 1
+        return self.out
+
+    def device_state(self) -> dict:
+        return self.scene._ctx.state_get()

@@ -307,3 +307,27 @@ def test_async_host_delivery(pkg):
     torch.cuda.synchronize()
     assert torch.equal(hosts[4 % 2], expect[4].cpu())
     assert torch.equal(hosts[3 % 2], expect[3].cpu())
+
+
+def test_captured_step_matches_eager(pkg):
+    """CUDA-graph replay (device step state) == eager render_pipeline, bitwise, incl. latency ring."""
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    case = casefile.load(os.path.join(GOLDEN, "render_cfg2_slice.npz"))
+    s_eager, s_graph = casefile.build_scene(case, pkg), casefile.build_scene(case, pkg)
+    cfg = pkg.SensorConfig(seed=6)
+    n = s_eager.num_envs
+    delays = np.array([0.0, 0.02, 0.05, 0.1, 0.013, 0.07, 0.04, 0.2])[:n]
+    dt = 0.02
+    fb_e, fb_g = pkg.FrameBuffer(capacity=4), pkg.FrameBuffer(capacity=4)
+    cap = CapturedStep(s_graph, sensor=cfg, frame_buffer=fb_g, delays=delays, dt=dt, first_step=3)
+    rng = np.random.default_rng(1)
+    for k in range(3, 10):
+        pos = (case["body_pos"] + rng.normal(0, 0.01, case["body_pos"].shape)).astype(np.float32)
+        s_eager.set_body_poses(pos, case["body_rot"])
+        s_graph.body_positions.copy_(torch.from_numpy(pos))
+        ref = pkg.render_pipeline(s_eager, sensor=cfg, step=k, frame_buffer=fb_e, timestamp=k * dt, delays=delays)
+        got = cap.replay()
+        assert torch.equal(got, ref), f"step {k}"
+        assert fb_g._times == fb_e._times and fb_g._slots == fb_e._slots
+    st = cap.device_state()
+    assert st["next_step"] == 10 and st["times"] == fb_e._times and st["order"] == fb_e._slots

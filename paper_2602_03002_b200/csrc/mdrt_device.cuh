@@ -14,8 +14,12 @@ namespace mdrt {
 
 constexpr int kStack = 24;          // == kMaxDepth of the builder
 constexpr int kBlock = 128;         // threads per render block (4 warps, 4 tiles)
-constexpr int kTileW = 8;           // a warp renders an 8x4 pixel tile of one view
-constexpr int kTileH = 4;
+#ifndef MDRT_TILE_W
+#define MDRT_TILE_W 8
+#endif
+constexpr int kTileW = MDRT_TILE_W;  // a warp renders a kTileW x kTileH pixel tile of one view
+constexpr int kTileH = 32 / kTileW;
+static_assert(kTileW * kTileH == 32 && (kTileW & (kTileW - 1)) == 0, "tile must be 32 pixels, power-of-2 wide");
 constexpr int kExit = INT32_MIN;    // traversal stack sentinel
 constexpr float kRayEps = 1e-6f;    // RAY_EPSILON (bvh.py:30): hits need t > 1e-6
 constexpr float kBaryEps = 1e-5f;   // fp32 watertightness margin on barycentrics

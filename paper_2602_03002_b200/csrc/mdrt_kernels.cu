@@ -278,7 +278,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     const uint32_t ty = tile / static_cast<uint32_t>(p.tiles_x);
     const uint32_t tx = tile - ty * static_cast<uint32_t>(p.tiles_x);
     const int px = static_cast<int>(tx) * kTileW + (lane & (kTileW - 1));
-    const int py = static_cast<int>(ty) * kTileH + (lane >> 3);
+    const int py = static_cast<int>(ty) * kTileH + lane / kTileW;
     const bool active = px < p.W && py < p.H;
     const uint32_t e = view / static_cast<uint32_t>(p.C);
     const uint32_t c = view - e * static_cast<uint32_t>(p.C);
@@ -363,12 +363,14 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     // ---- K3: fused epilogue ----
     float val = z;
     if (p.sensor) {
-        // lanes 0-3 hash the tile's 4 rows of the uniform stream, lanes 4-7 of the
-        // normal stream; everyone picks its row's prefixes by shuffle
-        const unsigned long long rowh = absorb((lane & 4) ? V.hn : V.hu,
-                                               static_cast<unsigned long long>(ty * kTileH + (lane & 3)));
-        const unsigned long long ru = __shfl_sync(0xffffffffu, rowh, lane >> 3);
-        const unsigned long long rn = __shfl_sync(0xffffffffu, rowh, 4 + (lane >> 3));
+        // a few lanes hash the tile's rows of the uniform and of the normal stream;
+        // everyone picks its row's prefixes by shuffle
+        // (lanes 0..kTileH-1: uniform stream rows, kTileH..2*kTileH-1: normal stream rows)
+        const int hl = lane % (2 * kTileH);
+        const unsigned long long rowh = absorb(hl >= kTileH ? V.hn : V.hu,
+                                               static_cast<unsigned long long>(ty * kTileH + hl % kTileH));
+        const unsigned long long ru = __shfl_sync(0xffffffffu, rowh, lane / kTileW);
+        const unsigned long long rn = __shfl_sync(0xffffffffu, rowh, kTileH + lane / kTileW);
         val = sensor_apply(z, ru, rn, static_cast<unsigned long long>(px), p.noise_scale, p.dropout_p,
                            p.fill[c], p.dmax64[c]);
     }

@@ -160,41 +160,50 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     return r;
 }
 
-// Returns the nearest hit parameter t in (1e-6, tmax] or +inf when nothing
-// is hit (the caller then keeps its bound; numba_backend.py:206-208).
-// Ordered closest-hit traversal: at an inner record both child boxes are
-// slab-tested, the nearer hit child is descended and the farther one pushed
-// together with its entry distance, so pops whose entry lies beyond the best
-// hit so far are discarded without fetching the record.
-// `stack` points at this thread's column of a [kStack][kBlock] shared array.
+// Resumable closest-hit traversal of one ray through one tree (numba_backend.py:
+// 124-152 semantics, fp32, ordered). Each inner record holds both children's
+// boxes: the nearer hit child is descended and the farther one pushed with its
+// entry distance, so pops beyond the best hit so far are skipped without a
+// fetch. State lives in registers plus this thread's column of a
+// [kStack][kBlock] shared array of packed {ref, entry distance} slots.
+// round() advances to the next leaf, tests it and pops; it returns true when
+// the ray is finished, so callers can interleave work between rounds.
 template <bool COUNT>
-__device__ __forceinline__ float trace(const float4* __restrict__ nodes, const float4* __restrict__ tris,
-                                       int32_t root, float ox, float oy, float oz, float dx, float dy,
-                                       float dz, float tmax, int2* __restrict__ stack,
-                                       TraceCounters& ctr) {
-    // zero direction components: a huge reciprocal turns the slab into a
-    // containment test like _slab_hit's d == 0 branch (numba_backend.py:76-78)
-    const float tiny = 1e-30f;
-    const float idx = rcp_approx(fabsf(dx) > tiny ? dx : copysignf(tiny, dx));
-    const float idy = rcp_approx(fabsf(dy) > tiny ? dy : copysignf(tiny, dy));
-    const float idz = rcp_approx(fabsf(dz) > tiny ? dz : copysignf(tiny, dz));
-    const float oxd = ox * idx, oyd = oy * idy, ozd = oz * idz;
+struct Traversal {
+    float ox, oy, oz, dx, dy, dz;
+    float idx, idy, idz, oxd, oyd, ozd;
+    float best;
+    bool hit;
+    int32_t ref;
+    int2* top;
+    int2* bottom;
 
-    float best = tmax;
-    bool hit = false;
-    // stack entries {ref, entry distance} in one 8-byte shared slot per level;
-    // `top` walks this thread's column ([kStack][kBlock] layout, conflict-free)
-    int2* top = stack;
-    int2* const bottom = stack;
-    auto pop = [&]() -> int32_t {
+    __device__ __forceinline__ void init(int32_t root, float ox_, float oy_, float oz_, float dx_, float dy_,
+                                         float dz_, float tmax, int2* stack) {
+        ox = ox_; oy = oy_; oz = oz_; dx = dx_; dy = dy_; dz = dz_;
+        // zero direction components: a huge reciprocal turns the slab into a
+        // containment test like _slab_hit's d == 0 branch (numba_backend.py:76-78)
+        const float tiny = 1e-30f;
+        idx = rcp_approx(fabsf(dx) > tiny ? dx : copysignf(tiny, dx));
+        idy = rcp_approx(fabsf(dy) > tiny ? dy : copysignf(tiny, dy));
+        idz = rcp_approx(fabsf(dz) > tiny ? dz : copysignf(tiny, dz));
+        oxd = ox * idx; oyd = oy * idy; ozd = oz * idz;
+        best = tmax;
+        hit = false;
+        ref = root;
+        top = bottom = stack;
+    }
+
+    __device__ __forceinline__ int32_t pop() {
         while (top != bottom) {
             top -= kBlock;
             const int2 e = *top;
             if (__int_as_float(e.y) <= best) return e.x;
         }
         return kExit;
-    };
-    auto test_leaf = [&](int32_t lref) {
+    }
+
+    __device__ __forceinline__ void test_leaf(const float4* __restrict__ tris, int32_t lref, TraceCounters& ctr) {
         // leaf: ~((first << 3) | (count - 1))
         const int32_t v = ~lref;
         const int32_t first = v >> 3;
@@ -225,9 +234,10 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
                 hit = true;
             }
         }
-    };
-    int32_t ref = root;
-    while (true) {
+    }
+
+    __device__ __forceinline__ bool round(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                          TraceCounters& ctr) {
         while (ref >= 0) {
             const float4* n = nodes + 4 * static_cast<int64_t>(ref);
             float4 bx, by, bz, rff;
@@ -257,13 +267,28 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
             } else {
                 ref = pop();
             }
-                }
-        if (ref == kExit) break;
-        test_leaf(ref);
+        }
+        if (ref == kExit) return true;
+        test_leaf(tris, ref, ctr);
         ref = pop();
-        if (ref == kExit) break;
+        return ref == kExit;
     }
-    return hit ? best : __int_as_float(0x7f800000);
+
+    // nearest hit t in (1e-6, tmax], or +inf when nothing was hit (the caller then
+    // keeps its bound; numba_backend.py:206-208)
+    __device__ __forceinline__ float result() const { return hit ? best : __int_as_float(0x7f800000); }
+};
+
+template <bool COUNT>
+__device__ __forceinline__ float trace(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                       int32_t root, float ox, float oy, float oz, float dx, float dy,
+                                       float dz, float tmax, int2* __restrict__ stack,
+                                       TraceCounters& ctr) {
+    Traversal<COUNT> tv;
+    tv.init(root, ox, oy, oz, dx, dy, dz, tmax, stack);
+    while (!tv.round(nodes, tris, ctr)) {
+    }
+    return tv.result();
 }
 
 }  // namespace mdrt

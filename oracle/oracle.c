@@ -22,6 +22,7 @@
  *   orc_noise_dropout    sensor.py:55-82           (apply_noise_dropout)
  *   orc_frame_select     sensor.py:133-150         (FrameBuffer.fetch_delayed[_batch])
  *   orc_downsample_min   sensor.py:85-100          (downsample_min)
+ *   orc_rsm_apply        perception.py:169-202     (rsm_apply, random side masking)
  *
  * Parity of this restatement against the live reference is pinned by
  * tests/golden/make_golden.py (run where /root/reference exists) and
@@ -439,4 +440,29 @@ int orc_max_threads(void) {
 #else
     return 1;
 #endif
+}
+
+/* rsm_apply: perception.py:169-202. Side bands of k = int(f * W) columns per
+ * side (mode 0: none, 1: f_small, 2: f_large; k passed per mode) are
+ * overwritten with uniform(key, step, env, cam, row, col, low, high_c) cast to
+ * f32; all other pixels are copied bit-identically. env = env_offset + e. */
+void orc_rsm_apply(const float *depth, int64_t N, int64_t C, int64_t H, int64_t W, const int32_t *modes,
+                   const int64_t *k_for_mode, uint64_t key, int64_t step, int64_t env_offset, double low,
+                   const double *high, float *out) {
+    memcpy(out, depth, sizeof(float) * (size_t)(N * C * H * W));
+    for (int64_t e = 0; e < N; ++e)
+        for (int64_t c = 0; c < C; ++c) {
+            int64_t k = k_for_mode[modes[e * C + c]];
+            if (k == 0) continue;
+            uint64_t hc = orc_absorb(orc_absorb(orc_absorb(key, (uint64_t)step), (uint64_t)(env_offset + e)),
+                                     (uint64_t)c);
+            for (int64_t y = 0; y < H; ++y) {
+                uint64_t hy = orc_absorb(hc, (uint64_t)y);
+                for (int64_t x = 0; x < W; ++x) {
+                    if (x >= k && x < W - k) continue;
+                    double u = unit_closed_open(orc_absorb(hy, (uint64_t)x));
+                    out[((e * C + c) * H + y) * W + x] = (float)(low + (high[c] - low) * u);
+                }
+            }
+        }
 }

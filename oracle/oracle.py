@@ -20,6 +20,7 @@ module is the numpy glue that restates the reference's host-side steps
 * ``sample_latencies``    sensor.py:153-158
 * ``frame_select``        sensor.py:133-150 (C: orc_frame_select)
 * ``downsample_min``      sensor.py:85-100  (C: orc_downsample_min)
+* ``rsm_*``               perception.py:150-202 (C: orc_rsm_apply; modes via categorical)
 
 Pinned against the live reference by tests/golden/make_golden.py.
 """
@@ -91,6 +92,9 @@ def lib():
             L.orc_downsample_min.restype = None
             L.orc_downsample_min.argtypes = [_fp, _i64, _i64, _i64, _i64, _fp]
             L.orc_max_threads.restype = ctypes.c_int
+            L.orc_rsm_apply.restype = None
+            L.orc_rsm_apply.argtypes = [_fp, _i64, _i64, _i64, _i64, _i32p, _i64p, _u64, _i64, _i64,
+                                        ctypes.c_double, _dp, _fp]
             _lib = L
     return _lib
 
@@ -411,4 +415,32 @@ def downsample_min(depth, factor):
     planes = int(np.prod(depth.shape[:-2]))
     out = np.empty(depth.shape[:-2] + (h // factor, w // factor), np.float32)
     lib().orc_downsample_min(_p(depth, _fp), planes, h, w, factor, _p(out, _fp))
+    return out
+
+
+def categorical(key, probs, *counters):
+    """rng.py:102-116."""
+    probs = np.asarray(probs, dtype=np.float64)
+    edges = np.cumsum(probs)
+    u = np.asarray(uniform(key, *counters)) * edges[-1]
+    return np.minimum(np.searchsorted(edges, u, side="right"), len(probs) - 1).astype(np.int64)
+
+
+def rsm_sample_modes(probs, seed, num_envs, num_cameras, episode=0):
+    """perception.py:150-157."""
+    return categorical(stream_key(seed, "rsm-mode"), probs, episode, np.arange(num_envs).reshape(-1, 1),
+                       np.arange(num_cameras).reshape(1, -1))
+
+
+def rsm_apply(depth, modes, *, f_small, f_large, fill_low, fill_high, seed, d_max, step=0, env_offset=0):
+    """perception.py:169-202 (k = int(f * W) per side, fill uniform [fill_low, fill_high or d_max])."""
+    depth = np.ascontiguousarray(depth, np.float32)
+    n, c, h, w = depth.shape
+    modes = np.ascontiguousarray(modes, np.int32)
+    high = np.ascontiguousarray(np.broadcast_to(np.asarray(d_max if fill_high is None else fill_high,
+                                                           np.float64), (c,)))
+    ks = np.array([0, int(f_small * w), int(f_large * w)], np.int64)
+    out = np.empty_like(depth)
+    lib().orc_rsm_apply(_p(depth, _fp), n, c, h, w, _p(modes, _i32p), _p(ks, _i64p), stream_key(seed, "rsm-fill"),
+                        int(step), int(env_offset), float(fill_low), _p(high, _dp), _p(out, _fp))
     return out

@@ -230,6 +230,16 @@ def main():
     # camera offsets (sensor.py:183-211)
     p, q, f = md.sample_camera_offsets(md.CameraRandomization(seed=4), 16, 2, episode=1)
     sens["camoff_pos"], sens["camoff_rot"], sens["camoff_fov"] = p, q, f
+    # random side masking (perception.py:150-202)
+    from multidepth import perception as mp
+    rcfg = mp.RsmConfig(seed=3)
+    sens["rsm_modes_stones"] = mp.rsm_sample_modes(rcfg, "stepping_stones", 64, 2, episode=1)
+    rdepth = g.uniform(0.5, 5.0, size=(4, 2, 27, 48)).astype(np.float32)
+    rmodes = np.array([[0, 1], [2, 0], [1, 2], [2, 2]])
+    sens["rsm_depth"], sens["rsm_modes"] = rdepth, rmodes
+    sens["rsm_out_s5"] = mp.rsm_apply(rdepth, rmodes, rcfg, d_max=np.array([6.0, 8.0]), step=5)
+    rcfg2 = mp.RsmConfig(seed=4, fill_high=4.0, f_small=0.1, f_large=0.3)
+    sens["rsm_out2_s0"] = mp.rsm_apply(rdepth, rmodes, rcfg2, d_max=np.array([6.0, 8.0]), step=0)
     np.savez_compressed(os.path.join(HERE, "sensor.npz"), **sens)
 
     # early-termination-off render of rand_noet

@@ -133,3 +133,14 @@ def test_oracle_latency_selection_bit_exact(oracle, sens):
 def test_oracle_latencies_and_downsample(oracle, sens):
     assert np.array_equal(oracle.sample_latencies(0.1, 5, 100, episode=2), sens["latencies_ep2"])
     assert np.array_equal(oracle.downsample_min(sens["ds_in"], 5), sens["ds_out"])
+
+
+def test_oracle_rsm_matches_reference(oracle, sens):
+    """Random side masking (perception.py:150-202): modes and fills bit-exact."""
+    assert np.array_equal(oracle.rsm_sample_modes((0.6, 0.3, 0.1), 3, 64, 2, episode=1), sens["rsm_modes_stones"])
+    out = oracle.rsm_apply(sens["rsm_depth"], sens["rsm_modes"], f_small=0.125, f_large=0.25, fill_low=0.3,
+                           fill_high=None, seed=3, d_max=[6.0, 8.0], step=5)
+    assert np.array_equal(out, sens["rsm_out_s5"])
+    out2 = oracle.rsm_apply(sens["rsm_depth"], sens["rsm_modes"], f_small=0.1, f_large=0.3, fill_low=0.3,
+                            fill_high=4.0, seed=4, d_max=[6.0, 8.0], step=0)
+    assert np.array_equal(out2, sens["rsm_out2_s0"])

@@ -43,6 +43,7 @@ extern "C" {
 #define MDRT_PHASE_PROLOGUE 0x20   /* launch only the per-view prologue (timing); neither phase flag = both */
 #define MDRT_PHASE_TRACE 0x40      /* launch only the traversal kernel (uses the last prologue's records)  */
 #define MDRT_COUNT_DETAIL 0x80     /* with MDRT_COUNT: counters has 4 slots (+ link node fetches, link traversals) */
+#define MDRT_RSM 0x200             /* random side masking of the output (perception.py:169-202)             */
 #define MDRT_DEVICE_STATE 0x100    /* step, timestamp, RNG prefix and ring push come from the context's device
                                       state (mdrt_state_set), advanced on the device at the start of the call:
                                       the call is then CUDA-graph capturable and replayable with no host args */
@@ -109,6 +110,13 @@ typedef struct {
     float *out_clean;          /* (N,C,H,W) clean range depth, or NULL                */
     float *out;                /* (N,C,H,W) final output (sensor/latency applied)     */
     unsigned long long *counters; /* (2,) device [node fetches, triangle tests] or NULL; (4,) with MDRT_COUNT_DETAIL */
+
+    /* random side masking: rsm_apply (perception.py:169-202) applied to `out` */
+    const int32_t *rsm_modes;  /* (N,C) mode per view (0 none, 1 small, 2 large), device */
+    int32_t rsm_k1, rsm_k2;    /* columns masked per side for modes 1 and 2 (int(f * W))  */
+    uint64_t rsm_key;          /* rng.stream_key(seed, "rsm-fill")                        */
+    double rsm_fill_low;       /* fill ~ U[fill_low, fill_high[c])                        */
+    const double *rsm_fill_high; /* HOST (C,), NULL -> d_max                              */
 } mdrt_step_args;
 
 /* ---- library ---------------------------------------------------------- */
@@ -152,9 +160,9 @@ int mdrt_render(mdrt_ctx *ctx, const mdrt_step_args *args, void *stream);
  * `now` into the ring (sensor.py:122-131). times/order: HOST (count,) current
  * ring content, oldest first. Also reserves per-step scratch for num_envs so
  * that later calls allocate nothing (capture-safe). Synchronous. */
-int mdrt_state_set(mdrt_ctx *ctx, int32_t num_envs, uint64_t sensor_key, double t0, double dt,
-                   int64_t next_step, int32_t ring_slots, const double *times, const int32_t *order,
-                   int32_t count);
+int mdrt_state_set(mdrt_ctx *ctx, int32_t num_envs, uint64_t sensor_key, uint64_t rsm_key, double t0,
+                   double dt, int64_t next_step, int32_t ring_slots, const double *times,
+                   const int32_t *order, int32_t count);
 /* Read back the device step state (next_step, now, write_slot, count, times, order). */
 int mdrt_state_get(mdrt_ctx *ctx, int64_t *next_step, double *now, int32_t *write_slot, int32_t *count,
                    double *times, int32_t *order);
@@ -175,6 +183,14 @@ int mdrt_gather_delayed(const float *const *frames, int32_t R, const int32_t *sl
  * times, now - delays[e]) - 1, 0)]. times/order: HOST (K,), K <= 32. */
 int mdrt_select_slots(const double *times, const int32_t *order, int32_t K, double now,
                       const double *delays, int32_t *slot, int64_t N, void *stream);
+
+/* rsm_apply (perception.py:169-202) on an existing (N,C,H,W) tensor: side bands of
+ * k[mode] columns get U[fill_low, fill_high[c]) from the "rsm-fill" stream keyed
+ * (step, env_offset + e, c, row, col); other pixels are copied. modes: (N,C)
+ * device; k: HOST (3,); fill_high: HOST (C,). */
+int mdrt_rsm_apply(const float *in, float *out, int32_t N, int32_t C, int32_t H, int32_t W,
+                   const int32_t *modes, const int32_t *k, uint64_t key, int64_t step, int64_t env_offset,
+                   double fill_low, const double *fill_high, void *stream);
 
 /* downsample_min (sensor.py:85-100): block minimum over trailing (H,W). */
 int mdrt_downsample_min(const float *in, float *out, int64_t planes, int32_t H, int32_t W,

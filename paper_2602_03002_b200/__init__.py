@@ -19,7 +19,9 @@ from .kernels import BACKENDS, default_backend, resolve_threads
 from .sensor import (SensorConfig, CameraRandomization, FrameBuffer, apply_noise_dropout,
                      downsample_min, sample_latencies, sample_camera_offsets, randomize_scene_cameras,
                      randomized_camera)
-from .pipeline import render_pipeline
+from .perception import (RsmConfig, RSM_MODES, DEFAULT_RSM_PROBS, rsm_sample_modes, rsm_mask_columns,
+                         rsm_apply)
+from .pipeline import CapturedStep, render_pipeline
 
 __version__ = "0.1.0"
 
@@ -33,5 +35,6 @@ __all__ = [
     "BACKENDS", "default_backend", "resolve_threads",
     "SensorConfig", "CameraRandomization", "FrameBuffer", "apply_noise_dropout", "downsample_min",
     "sample_latencies", "sample_camera_offsets", "randomize_scene_cameras", "randomized_camera",
-    "render_pipeline", "__version__",
+    "RsmConfig", "RSM_MODES", "DEFAULT_RSM_PROBS", "rsm_sample_modes", "rsm_mask_columns", "rsm_apply",
+    "render_pipeline", "CapturedStep", "__version__",
 ]

@@ -29,6 +29,7 @@ PHASE_PROLOGUE = 0x20
 PHASE_TRACE = 0x40
 COUNT_DETAIL = 0x80
 DEVICE_STATE = 0x100
+RSM = 0x200
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -77,6 +78,12 @@ class StepArgs(ctypes.Structure):
         ("out_clean", ctypes.c_void_p),
         ("out", ctypes.c_void_p),
         ("counters", ctypes.c_void_p),
+        ("rsm_modes", ctypes.c_void_p),
+        ("rsm_k1", ctypes.c_int32),
+        ("rsm_k2", ctypes.c_int32),
+        ("rsm_key", ctypes.c_uint64),
+        ("rsm_fill_low", ctypes.c_double),
+        ("rsm_fill_high", _c_dp),
     ]
 
 
@@ -125,8 +132,12 @@ def lib():
                                                    ctypes.c_int32, vp]),
             "mdrt_bvh_check": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64, _c_i64p]),
             "mdrt_probe_read": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp]),
-            "mdrt_state_set": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
-                                              ctypes.c_int64, ctypes.c_int32, _c_dp, _c_i32p, ctypes.c_int32]),
+            "mdrt_state_set": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_int64, ctypes.c_int32, _c_dp, _c_i32p,
+                                              ctypes.c_int32]),
+            "mdrt_rsm_apply": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              vp, _c_i32p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_double, _c_dp, vp]),
             "mdrt_state_get": (ctypes.c_int, [vp, _c_i64p, _c_dp, _c_i32p, _c_i32p, _c_dp, _c_i32p]),
             "mdrt_sync": (ctypes.c_int, [vp]),
         }
@@ -142,7 +153,7 @@ def lib():
 EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_create", "mdrt_destroy",
            "mdrt_add_body", "mdrt_set_terrain", "mdrt_set_cameras", "mdrt_commit", "mdrt_get_stats",
            "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
-           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_sync")
+           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_sync")
 
 
 def check(rc: int) -> None:
@@ -233,11 +244,12 @@ class Context:
     def sync(self) -> None:
         check(lib().mdrt_sync(self._ptr))
 
-    def state_set(self, num_envs, key, t0, dt, next_step, ring_slots, times, order) -> None:
+    def state_set(self, num_envs, key, t0, dt, next_step, ring_slots, times, order, rsm_key=0) -> None:
         import numpy as np
         t = np.ascontiguousarray(times, dtype=np.float64)
         o = np.ascontiguousarray(order, dtype=np.int32)
-        check(lib().mdrt_state_set(self._ptr, int(num_envs), int(key), float(t0), float(dt), int(next_step),
+        check(lib().mdrt_state_set(self._ptr, int(num_envs), int(key), int(rsm_key), float(t0), float(dt),
+                                   int(next_step),
                                    int(ring_slots), dptr(t), o.ctypes.data_as(_c_i32p), len(t)))
 
     def state_get(self) -> dict:

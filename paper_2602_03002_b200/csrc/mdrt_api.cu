@@ -351,6 +351,17 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         pp.hn_step = absorb(absorb(key, 1ULL), st);
         pp.latency = latency;
         pp.state = dstate ? ctx->state.ptr : nullptr;
+        const bool rsm = (a->flags & MDRT_RSM) != 0;
+        if (rsm) {
+            need(a->rsm_modes != nullptr, "rsm_modes is NULL with MDRT_RSM");
+            need(a->rsm_k1 >= 0 && a->rsm_k2 >= 0 && 2 * a->rsm_k1 <= ctx->W && 2 * a->rsm_k2 <= ctx->W,
+                 "rsm column counts out of range");
+            pp.rsm_modes = a->rsm_modes;
+            pp.rsm_k[0] = 0;
+            pp.rsm_k[1] = a->rsm_k1;
+            pp.rsm_k[2] = a->rsm_k2;
+            pp.hr_step = absorb(a->rsm_key, static_cast<unsigned long long>(a->step));
+        }
         if (latency && !dstate) {
             pp.ring_count = a->ring_count;
             pp.write_slot = a->write_slot;
@@ -409,6 +420,9 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.counters = a->counters;
         rp.count_detail = (a->flags & MDRT_COUNT_DETAIL) != 0;
         rp.state = dstate ? ctx->state.ptr : nullptr;
+        rp.rsm = rsm;
+        rp.rsm_low = a->rsm_fill_low;
+        for (int c = 0; c < C; ++c) rp.rsm_high[c] = a->rsm_fill_high ? a->rsm_fill_high[c] : ctx->rigs[c].d_max;
         ctx->tile_counter.reserve(1);
         rp.tile_counter = ctx->tile_counter.ptr;
         const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;
@@ -419,8 +433,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
     });
 }
 
-int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, double t0, double dt, int64_t next_step,
-                   int32_t ring_slots, const double* times, const int32_t* order, int32_t count) {
+int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, uint64_t rsm_key, double t0, double dt,
+                   int64_t next_step, int32_t ring_slots, const double* times, const int32_t* order, int32_t count) {
     return guarded([&] {
         need(ctx != nullptr, "ctx is NULL");
         if (!ctx->committed) throw StateError("mdrt_commit first");
@@ -431,6 +445,7 @@ int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, double 
         ctx->use_device();
         StepState st{};
         st.key = sensor_key;
+        st.rsm_key = rsm_key;
         st.next_step = next_step;
         st.t0 = t0;
         st.dt = dt;
@@ -494,6 +509,32 @@ int mdrt_noise_dropout(const float* depth, float* out, int32_t N, int32_t C, int
         const int64_t total = static_cast<int64_t>(N) * C * H * W;
         if (total == 0) return;
         launch_noise(p, total, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int mdrt_rsm_apply(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t W, const int32_t* modes,
+                   const int32_t* k, uint64_t key, int64_t step, int64_t env_offset, double fill_low,
+                   const double* fill_high, void* stream) {
+    return guarded([&] {
+        need(in && out && modes && k && fill_high, "NULL argument");
+        need(N >= 0 && C >= 1 && C <= 64 && H >= 1 && W >= 1, "bad shape");
+        RsmParams p{};
+        p.in = in;
+        p.out = out;
+        p.modes = modes;
+        p.N = N; p.C = C; p.H = H; p.W = W;
+        p.env_offset = env_offset;
+        for (int i = 0; i < 3; ++i) {
+            need(k[i] >= 0 && 2 * k[i] <= W, "mask columns out of range");
+            p.k[i] = k[i];
+        }
+        p.hr_step = absorb(key, static_cast<unsigned long long>(step));
+        p.low = fill_low;
+        for (int c = 0; c < C; ++c) p.high[c] = fill_high[c];
+        const int64_t total = static_cast<int64_t>(N) * C * H * W;
+        if (total == 0) return;
+        launch_rsm(p, total, static_cast<cudaStream_t>(stream));
         CK(cudaGetLastError());
     });
 }

@@ -52,7 +52,10 @@ struct alignas(16) ViewRec {
     int32_t pad0;
     unsigned long long hu; // rng prefix absorb(..step, env, cam) of the uniform stream
     unsigned long long hn; // same for the normal stream
-    float pad1[8];
+    unsigned long long hr; // rsm-fill stream prefix absorb(absorb(absorb(key, step), env), cam)
+    int32_t rsm_k;         // side-mask columns per side for this view (0: none)
+    int32_t pad2;
+    float pad1[4];
 };
 static_assert(sizeof(ViewRec) == 128, "ViewRec must be 128 B");
 

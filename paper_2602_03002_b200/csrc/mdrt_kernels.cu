@@ -246,6 +246,9 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
         const StepState* st = p.state;
         v.hu = absorb(absorb(st ? st->hu_step : p.hu_step, genv), static_cast<unsigned long long>(c));
         v.hn = absorb(absorb(st ? st->hn_step : p.hn_step, genv), static_cast<unsigned long long>(c));
+        v.rsm_k = p.rsm_modes ? p.rsm_k[min(max(p.rsm_modes[view], 0), 2)] : 0;
+        v.hr = absorb(absorb(st ? st->hr_step : p.hr_step, genv), static_cast<unsigned long long>(c));
+        v.pad2 = 0;
         if (p.latency) {
             // bisect_right(times, now - delay) - 1, clamped at 0 (sensor.py:138-139)
             const double* times = st ? st->times : p.ring_times;
@@ -264,7 +267,7 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
             v.read_slot = slot == wslot ? -1 : slot;
             if (c == 0 && p.read_slot_out) p.read_slot_out[e] = slot;
         }
-        for (int i = 0; i < 8; ++i) v.pad1[i] = 0.f;
+        for (int i = 0; i < 4; ++i) v.pad1[i] = 0.f;
         p.views[view] = v;
     }
 }
@@ -385,6 +388,15 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const int rs = V.read_slot;
         if (rs >= 0) val = p.ring[static_cast<int64_t>(rs) * frame + o];
     }
+    if (p.rsm) {
+        // random side masking of the observation (perception.py:183-202)
+        const int k = V.rsm_k;
+        if (k > 0 && (px < k || px >= p.W - k)) {
+            const unsigned long long h = absorb(absorb(V.hr, static_cast<unsigned long long>(py)),
+                                                static_cast<unsigned long long>(px));
+            val = static_cast<float>(__dadd_rn(p.rsm_low, __dmul_rn(p.rsm_high[c] - p.rsm_low, unit53(h))));
+        }
+    }
     p.out[o] = val;
 }
 
@@ -425,6 +437,29 @@ static __global__ void noise_kernel(NoiseParams p) {
         absorb(absorb(absorb(p.hn_step, genv), static_cast<unsigned long long>(c)), static_cast<unsigned long long>(y));
     p.out[i] = sensor_apply(p.in[i], ru, rn, static_cast<unsigned long long>(x), p.noise_scale, p.dropout_p,
                             p.fill[c], p.dmax[c]);
+}
+
+static __global__ void rsm_kernel(RsmParams p) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
+    if (i >= total) return;
+    const int x = static_cast<int>(i % p.W);
+    const int64_t r = i / p.W;
+    const int y = static_cast<int>(r % p.H);
+    const int64_t ec = r / p.H;
+    const int c = static_cast<int>(ec % p.C);
+    const int64_t e = ec / p.C;
+    const int k = p.k[min(max(p.modes[ec], 0), 2)];
+    float v = p.in[i];
+    if (k > 0 && (x < k || x >= p.W - k)) {
+        const unsigned long long h =
+            absorb(absorb(absorb(absorb(p.hr_step, static_cast<unsigned long long>(p.env_offset + e)),
+                                 static_cast<unsigned long long>(c)),
+                          static_cast<unsigned long long>(y)),
+                   static_cast<unsigned long long>(x));
+        v = static_cast<float>(__dadd_rn(p.low, __dmul_rn(p.high[c] - p.low, unit53(h))));
+    }
+    p.out[i] = v;
 }
 
 static __global__ void gather_kernel(GatherParams p) {
@@ -498,6 +533,7 @@ static __global__ void advance_kernel(StepState* st) {
     st->now = st->t0 + static_cast<double>(k) * st->dt;
     st->hu_step = absorb(absorb(st->key, 0ULL), static_cast<unsigned long long>(k));
     st->hn_step = absorb(absorb(st->key, 1ULL), static_cast<unsigned long long>(k));
+    st->hr_step = absorb(st->rsm_key, static_cast<unsigned long long>(k));
     if (st->ring_slots > 0) {
         int slot;
         if (st->ring_count < st->ring_slots) {
@@ -573,6 +609,10 @@ void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, c
 }
 
 void launch_advance(StepState* st, cudaStream_t s) { advance_kernel<<<1, 32, 0, s>>>(st); }
+
+void launch_rsm(const RsmParams& p, int64_t total, cudaStream_t s) {
+    rsm_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);
+}
 
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s) {
     downsample_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);

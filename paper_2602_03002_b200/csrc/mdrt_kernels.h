@@ -19,6 +19,8 @@ struct StepState {
     int32_t ring_slots, ring_count, write_slot, pad;
     double times[32];             // retained timestamps, oldest first
     int32_t order[32];            // their ring slots
+    unsigned long long rsm_key;   // rng.stream_key(seed, "rsm-fill")
+    unsigned long long hr_step;   // absorb(rsm_key, k)
 };
 
 struct PrologueParams {
@@ -49,6 +51,10 @@ struct PrologueParams {
     LinkRec* links;
     unsigned int* reset_counter;  // render kernel's tile counter, zeroed here (prologue runs first)
     const StepState* state;       // non-null: step/ring/RNG fields come from device state
+    // random side masking (perception.py:169-202)
+    const int32_t* rsm_modes;     // (N, C) mode per view or NULL
+    int32_t rsm_k[3];             // columns per side for modes 0, 1, 2
+    unsigned long long hr_step;   // absorb(rsm key, step)
 };
 
 struct RenderParams {
@@ -75,6 +81,9 @@ struct RenderParams {
     unsigned int* tile_counter;   // persistent-warp work counter (zeroed per launch)
     int32_t count_detail;         // counters has 4 slots: + link node fetches, link traversals
     const StepState* state;       // non-null: ring write slot comes from device state
+    int32_t rsm;                  // apply side masking to the observation
+    double rsm_low;
+    double rsm_high[64];
 };
 
 struct NoiseParams {
@@ -86,6 +95,18 @@ struct NoiseParams {
     double noise_scale, dropout_p;
     double fill[64];
     double dmax[64];
+};
+
+struct RsmParams {
+    const float* in;
+    float* out;
+    const int32_t* modes;
+    int32_t N, C, H, W;
+    int64_t env_offset;
+    int32_t k[3];
+    unsigned long long hr_step;
+    double low;
+    double high[64];
 };
 
 struct GatherParams {
@@ -121,5 +142,6 @@ void launch_select(const SelectParams& p, int64_t n, cudaStream_t s);
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s);
 void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, cudaStream_t s);
 void launch_advance(StepState* st, cudaStream_t s);
+void launch_rsm(const RsmParams& p, int64_t total, cudaStream_t s);
 
 }  // namespace mdrt

@@ -22,7 +22,23 @@ import torch
 
 from . import _native
 from .scene import Scene
+from .perception import RsmConfig, _fill_high, _modes_tensor, rsm_mask_columns
 from .sensor import FrameBuffer, SensorConfig, _delays_tensor
+
+
+def _set_rsm(a, scene: Scene, rsm: RsmConfig, rsm_modes, keep: list) -> None:
+    if rsm_modes is None:
+        raise ValueError("rsm needs rsm_modes (N, C)")
+    m = _modes_tensor(rsm_modes, scene.num_envs, scene.num_cameras, scene.device)
+    high = _fill_high(rsm, scene.d_max_per_camera, scene.num_cameras)
+    keep += [m, high]
+    a.flags |= _native.RSM
+    a.rsm_modes = m.data_ptr()
+    a.rsm_k1 = rsm_mask_columns(rsm, 1, scene.width)
+    a.rsm_k2 = rsm_mask_columns(rsm, 2, scene.width)
+    a.rsm_key = rsm.fill_key
+    a.rsm_fill_low = float(rsm.fill_low)
+    a.rsm_fill_high = _native.dptr(high)
 
 
 def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: int = 0,
@@ -30,7 +46,8 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
                     delays=None, early_termination: bool = True, out: torch.Tensor | None = None,
                     clean_out: torch.Tensor | None = None,
                     counters: torch.Tensor | None = None,
-                    host_out: torch.Tensor | None = None) -> torch.Tensor:
+                    host_out: torch.Tensor | None = None, rsm: RsmConfig | None = None,
+                    rsm_modes=None) -> torch.Tensor:
     """One simulation step of the multi-depth pipeline; returns the observation (N,C,H,W).
 
     * ``sensor``: apply noise/dropout/clamp with counters (step, global env, cam, row, col).
@@ -39,6 +56,8 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     * ``clean_out``: optionally also store the noise-free range image.
     * ``host_out``: pinned CPU tensor that receives the observation asynchronously
       (side copy stream, overlaps the next step; ``scene.host_sync()`` before use).
+    * ``rsm`` + ``rsm_modes`` (N, C): random side masking of the observation
+      (perception.py:169-202), i.e. ``rsm_apply(obs, rsm_modes, rsm, step=step)``.
     """
     data = scene._new_frame(out)
     scene._guard_out(data)
@@ -47,6 +66,9 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
         scene._new_frame(clean_out)
         a.out_clean = clean_out.data_ptr()
     keep = []
+    a.step = int(step)
+    if rsm is not None:
+        _set_rsm(a, scene, rsm, rsm_modes, keep)
     if sensor is not None:
         a.flags |= _native.SENSOR
         a.noise_scale = float(sensor.noise_scale)
@@ -106,7 +128,8 @@ class CapturedStep:
 
     def __init__(self, scene: Scene, *, sensor: SensorConfig | None = None,
                  frame_buffer: FrameBuffer | None = None, delays=None, dt: float = 0.02, t0: float = 0.0,
-                 first_step: int = 0, out: torch.Tensor | None = None, early_termination: bool = True):
+                 first_step: int = 0, out: torch.Tensor | None = None, early_termination: bool = True,
+                 rsm: RsmConfig | None = None, rsm_modes=None):
         if frame_buffer is not None and (delays is None or not dt > 0):
             raise ValueError("frame_buffer needs delays and dt > 0")
         self.scene = scene
@@ -118,6 +141,8 @@ class CapturedStep:
         a.flags |= _native.DEVICE_STATE
         self._keep = []
         key = 0
+        if rsm is not None:
+            _set_rsm(a, scene, rsm, rsm_modes, self._keep)
         if sensor is not None:
             a.flags |= _native.SENSOR
             a.noise_scale = float(sensor.noise_scale)
@@ -144,7 +169,8 @@ class CapturedStep:
             a.ring_slots = frame_buffer.capacity
             a.delays = d.data_ptr()
             a.read_slot = frame_buffer._slot_buf.data_ptr()
-        scene._ctx.state_set(scene.num_envs, key, self.t0, self.dt, self.next_step, slots, times, order)
+        scene._ctx.state_set(scene.num_envs, key, self.t0, self.dt, self.next_step, slots, times, order,
+                             rsm_key=rsm.fill_key if rsm is not None else 0)
         self._args = a
         # warm the launch path (occupancy query) outside capture, then capture
         plain = scene._step_args(self.out, early_termination)

@@ -331,3 +331,33 @@ def test_captured_step_matches_eager(pkg):
         assert fb_g._times == fb_e._times and fb_g._slots == fb_e._slots
     st = cap.device_state()
     assert st["next_step"] == 10 and st["times"] == fb_e._times and st["order"] == fb_e._slots
+
+
+def test_rsm_matches_reference(pkg, sens):
+    """Random side masking (perception.py:150-202): modes and fills bit-exact vs reference goldens."""
+    cfg = pkg.RsmConfig(seed=3)
+    assert np.array_equal(pkg.rsm_sample_modes(cfg, "stepping_stones", 64, 2, episode=1), sens["rsm_modes_stones"])
+    out = pkg.rsm_apply(torch.from_numpy(sens["rsm_depth"]).cuda(), sens["rsm_modes"], cfg, d_max=[6.0, 8.0],
+                        step=5).cpu().numpy()
+    assert np.array_equal(out, sens["rsm_out_s5"])
+    cfg2 = pkg.RsmConfig(seed=4, fill_high=4.0, f_small=0.1, f_large=0.3)
+    out2 = pkg.rsm_apply(sens["rsm_depth"], sens["rsm_modes"], cfg2, d_max=[6.0, 8.0], step=0)
+    assert np.array_equal(out2, sens["rsm_out2_s0"])
+
+
+def test_fused_rsm_equals_standalone(pkg):
+    """render_pipeline(rsm=...) == rsm_apply(render_pipeline(...)), and the captured step agrees."""
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    case, scene = _case_scene(pkg, "render_cfg2_slice.npz")
+    sc2 = casefile.build_scene(case, pkg)
+    n, c = scene.num_envs, scene.num_cameras
+    sens_cfg = pkg.SensorConfig(seed=2)
+    rsm = pkg.RsmConfig(seed=7)
+    modes = pkg.rsm_sample_modes(rsm, "stairs_up", n, c, episode=0)
+    cap = CapturedStep(sc2, sensor=sens_cfg, rsm=rsm, rsm_modes=modes, first_step=4)
+    for s in range(4, 7):
+        fused = pkg.render_pipeline(scene, sensor=sens_cfg, step=s, rsm=rsm, rsm_modes=modes).clone()
+        plain = pkg.render_pipeline(scene, sensor=sens_cfg, step=s)
+        ref = pkg.rsm_apply(plain, modes, rsm, d_max=scene.d_max_per_camera, step=s)
+        assert torch.equal(fused, ref), f"step {s}"
+        assert torch.equal(cap.replay(), ref), f"captured step {s}"

@@ -158,3 +158,20 @@ def test_frame_buffer_host_bookkeeping():
         buf._reserve(5.0)
     with pytest.raises(ValueError):
         FrameBuffer(capacity=0)
+
+
+def test_rsm_host_side(sens):
+    from paper_2602_03002_b200.perception import RSM_MODES, RsmConfig, rsm_mask_columns, rsm_sample_modes
+    assert RSM_MODES == ("none", "small", "large")
+    cfg = RsmConfig()
+    assert [rsm_mask_columns(cfg, m, 48) for m in (0, 1, 2)] == [0, 6, 12]
+    assert rsm_mask_columns(cfg, 1, 30) == 3
+    assert np.array_equal(rsm_sample_modes(RsmConfig(seed=3), "stepping_stones", 64, 2, episode=1),
+                          sens["rsm_modes_stones"])
+    modes = rsm_sample_modes(RsmConfig(seed=0), "stepping_stones", 100_000, 1)
+    freqs = np.bincount(modes.ravel(), minlength=3) / modes.size
+    assert np.all(np.abs(freqs - np.array([0.6, 0.3, 0.1])) < 0.01)
+    with pytest.raises(KeyError):
+        cfg.probs_for("volcano")
+    with pytest.raises(ValueError):
+        RsmConfig(probs={"flat": (0.5, 0.5, 0.5)})

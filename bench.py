@@ -429,6 +429,14 @@ def main():
     e2e_ms = e0.elapsed_time(e1)
     h2d = pose_host[0][0].numel() * 4 + pose_host[0][1].numel() * 4
     d2h = host_obs[0].numel() * 4
+    # PCIe reference: one observation-sized pinned D2H copy alone (the e2e floor)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for i in range(5):
+        host_obs[i % 2].copy_(out, non_blocking=True)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    d2h_gbs = 5 * d2h / (c0.elapsed_time(c1) * 1e-3) / 1e9
 
     # ---- optional: step + NCCL gather of every rank's observation to rank 0 ----
     gather_ms = 0.0
@@ -508,7 +516,8 @@ def main():
                          "l2_frac": (achieved / l2_gbs) if l2_gbs else None},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms / args.steps,
+                    "ms_per_step": e2e_ms / args.steps, "d2h_alone_gbs": d2h_gbs,
+                    "d2h_floor_ms": d2h / (d2h_gbs * 1e9) * 1e3,
                     "how": "pinned-host poses H2D + fused pipeline + obs D2H (copy stream, double-buffered) "
                            "every step, L2 flush inside the timed loop, events around the whole loop"},
             "gpu_launches": 2 * args.steps,

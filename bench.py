@@ -416,6 +416,7 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    e2e_wall0 = time.perf_counter()
     for i in range(args.steps):
         flush.fill_(float(i))
         hp, hq = pose_host[i % P]
@@ -423,6 +424,7 @@ def main():
         md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf, timestamp=step_id[0] * dt,
                            delays=delays, out=outs[i % 2], host_out=host_obs[i % 2])
         step_id[0] += 1
+    e2e_host_ms = (time.perf_counter() - e2e_wall0) * 1e3   # host time to enqueue the loop
     stream.wait_event(scene._last_copy)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -521,6 +523,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "d2h_alone_gbs": d2h_gbs,
+                    "host_enqueue_ms_per_step": e2e_host_ms / args.steps,
                     "d2h_floor_ms": d2h / (d2h_gbs * 1e9) * 1e3,
                     "how": "pinned-host poses H2D + fused pipeline + obs D2H (copy stream, double-buffered) "
                            "every step, L2 flush inside the timed loop, events around the whole loop"},

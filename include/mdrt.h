@@ -117,6 +117,10 @@ typedef struct {
     uint64_t rsm_key;          /* rng.stream_key(seed, "rsm-fill")                        */
     double rsm_fill_low;       /* fill ~ U[fill_low, fill_high[c])                        */
     const double *rsm_fill_high; /* HOST (C,), NULL -> d_max                              */
+
+    /* fused downsample_min (sensor.py:85-100) of the final output */
+    float *ds_out;             /* (N,C,H/f,W/f) block minimum, or NULL; `out` may then be NULL */
+    int32_t ds_factor;         /* f; H and W must be divisible by f                          */
 } mdrt_step_args;
 
 /* ---- library ---------------------------------------------------------- */

@@ -84,6 +84,8 @@ class StepArgs(ctypes.Structure):
         ("rsm_key", ctypes.c_uint64),
         ("rsm_fill_low", ctypes.c_double),
         ("rsm_fill_high", _c_dp),
+        ("ds_out", ctypes.c_void_p),
+        ("ds_factor", ctypes.c_int32),
     ]
 
 

@@ -299,7 +299,11 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         if (!ctx->committed) throw StateError("mdrt_commit must precede mdrt_render");
         const int32_t N = a->num_envs, C = ctx->C, B = static_cast<int32_t>(ctx->bodies.size());
         need(N >= 1, "num_envs must be >= 1");
-        need(a->out != nullptr, "out is NULL");
+        need(a->out != nullptr || a->ds_out != nullptr, "out is NULL");
+        if (a->ds_out) {
+            need(a->ds_factor >= 1 && ctx->H % a->ds_factor == 0 && ctx->W % a->ds_factor == 0,
+                 "resolution not divisible by downsample factor");
+        }
         const bool seam = a->cam_pos != nullptr;
         need(!seam || a->cam_rot != nullptr, "cam_rot is NULL while cam_pos is set");
         need(B == 0 || (a->body_pos && a->body_rot), "body poses are NULL");
@@ -421,6 +425,12 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.count_detail = (a->flags & MDRT_COUNT_DETAIL) != 0;
         rp.state = dstate ? ctx->state.ptr : nullptr;
         rp.rsm = rsm;
+        rp.ds_out = reinterpret_cast<unsigned int*>(a->ds_out);
+        rp.ds_factor = a->ds_factor;
+        rp.ds_w = a->ds_out ? ctx->W / a->ds_factor : 0;
+        rp.ds_h = a->ds_out ? ctx->H / a->ds_factor : 0;
+        if (a->ds_out && !only_pro)   // +inf-like start value for the block minima (0x7f7f7f7f = 3.4e38)
+            CK(cudaMemsetAsync(a->ds_out, 0x7f, sizeof(float) * nviews * rp.ds_w * rp.ds_h, s));
         rp.rsm_low = a->rsm_fill_low;
         for (int c = 0; c < C; ++c) rp.rsm_high[c] = a->rsm_fill_high ? a->rsm_fill_high[c] : ctx->rigs[c].d_max;
         ctx->tile_counter.reserve(1);

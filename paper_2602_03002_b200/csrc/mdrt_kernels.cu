@@ -378,26 +378,38 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         val = sensor_apply(z, ru, rn, static_cast<unsigned long long>(px), p.noise_scale, p.dropout_p,
                            p.fill[c], p.dmax64[c]);
     }
-    if (!active) return;
-    const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
-    if (p.out_clean) p.out_clean[o] = z;
-    if (p.ring) {
-        const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
-        const int wslot = p.state ? p.state->write_slot : p.write_slot;
-        p.ring[static_cast<int64_t>(wslot) * frame + o] = val;
-        const int rs = V.read_slot;
-        if (rs >= 0) val = p.ring[static_cast<int64_t>(rs) * frame + o];
-    }
-    if (p.rsm) {
-        // random side masking of the observation (perception.py:183-202)
-        const int k = V.rsm_k;
-        if (k > 0 && (px < k || px >= p.W - k)) {
-            const unsigned long long h = absorb(absorb(V.hr, static_cast<unsigned long long>(py)),
-                                                static_cast<unsigned long long>(px));
-            val = static_cast<float>(__dadd_rn(p.rsm_low, __dmul_rn(p.rsm_high[c] - p.rsm_low, unit53(h))));
+    if (active) {
+        const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
+        if (p.out_clean) p.out_clean[o] = z;
+        if (p.ring) {
+            const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
+            const int wslot = p.state ? p.state->write_slot : p.write_slot;
+            p.ring[static_cast<int64_t>(wslot) * frame + o] = val;
+            const int rs = V.read_slot;
+            if (rs >= 0) val = p.ring[static_cast<int64_t>(rs) * frame + o];
         }
+        if (p.rsm) {
+            // random side masking of the observation (perception.py:183-202)
+            const int k = V.rsm_k;
+            if (k > 0 && (px < k || px >= p.W - k)) {
+                const unsigned long long h = absorb(absorb(V.hr, static_cast<unsigned long long>(py)),
+                                                    static_cast<unsigned long long>(px));
+                val = static_cast<float>(__dadd_rn(p.rsm_low, __dmul_rn(p.rsm_high[c] - p.rsm_low, unit53(h))));
+            }
+        }
+        if (p.out) p.out[o] = val;
     }
-    p.out[o] = val;
+    if (p.ds_out) {
+        // block-minimum downsample of the observation (sensor.py:85-100): lanes of
+        // the same f x f block combine by warp reduction, one atomicMin per block
+        // and warp (positive floats order like their bit patterns).
+        const int f = p.ds_factor;
+        const long long key = active ? (static_cast<long long>(view) * p.ds_h + py / f) * p.ds_w + px / f
+                                     : -1LL - lane;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const unsigned mn = __reduce_min_sync(grp, __float_as_uint(val));
+        if (active && lane == __ffs(grp) - 1) atomicMin(p.ds_out + key, mn);
+    }
 }
 
 // Persistent warps: each warp pulls 8x4 tiles from a global counter until the

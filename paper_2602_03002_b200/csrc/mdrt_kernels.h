@@ -81,6 +81,8 @@ struct RenderParams {
     unsigned int* tile_counter;   // persistent-warp work counter (zeroed per launch)
     int32_t count_detail;         // counters has 4 slots: + link node fetches, link traversals
     const StepState* state;       // non-null: ring write slot comes from device state
+    unsigned int* ds_out;         // (N, C, H/f, W/f) block-min of the observation (float bits) or NULL
+    int32_t ds_factor, ds_w, ds_h;
     int32_t rsm;                  // apply side masking to the observation
     double rsm_low;
     double rsm_high[64];

@@ -26,6 +26,18 @@ from .perception import RsmConfig, _fill_high, _modes_tensor, rsm_mask_columns
 from .sensor import FrameBuffer, SensorConfig, _delays_tensor
 
 
+def _set_downsample(a, scene: Scene, ds_out: torch.Tensor, f: int) -> None:
+    n, c, h, w = scene.frame_shape
+    if f < 1 or h % f or w % f:
+        raise ValueError(f"resolution {w}x{h} not divisible by downsample factor {f}")
+    shape = (n, c, h // f, w // f)
+    if (not isinstance(ds_out, torch.Tensor) or ds_out.device != scene.device or ds_out.dtype != torch.float32
+            or tuple(ds_out.shape) != shape or not ds_out.is_contiguous()):
+        raise ValueError(f"ds_out must be a contiguous float32 CUDA tensor of shape {shape}")
+    a.ds_out = ds_out.data_ptr()
+    a.ds_factor = int(f)
+
+
 def _set_rsm(a, scene: Scene, rsm: RsmConfig, rsm_modes, keep: list) -> None:
     if rsm_modes is None:
         raise ValueError("rsm needs rsm_modes (N, C)")
@@ -47,7 +59,8 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
                     clean_out: torch.Tensor | None = None,
                     counters: torch.Tensor | None = None,
                     host_out: torch.Tensor | None = None, rsm: RsmConfig | None = None,
-                    rsm_modes=None) -> torch.Tensor:
+                    rsm_modes=None, ds_out: torch.Tensor | None = None,
+                    downsample_factor: int = 5) -> torch.Tensor:
     """One simulation step of the multi-depth pipeline; returns the observation (N,C,H,W).
 
     * ``sensor``: apply noise/dropout/clamp with counters (step, global env, cam, row, col).
@@ -58,6 +71,8 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
       (side copy stream, overlaps the next step; ``scene.host_sync()`` before use).
     * ``rsm`` + ``rsm_modes`` (N, C): random side masking of the observation
       (perception.py:169-202), i.e. ``rsm_apply(obs, rsm_modes, rsm, step=step)``.
+    * ``ds_out`` (N, C, H/f, W/f): also write ``downsample_min(obs, f)``
+      (sensor.py:85-100) from the same kernel, f = ``downsample_factor``.
     """
     data = scene._new_frame(out)
     scene._guard_out(data)
@@ -67,6 +82,8 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
         a.out_clean = clean_out.data_ptr()
     keep = []
     a.step = int(step)
+    if ds_out is not None:
+        _set_downsample(a, scene, ds_out, downsample_factor)
     if rsm is not None:
         _set_rsm(a, scene, rsm, rsm_modes, keep)
     if sensor is not None:
@@ -129,7 +146,8 @@ class CapturedStep:
     def __init__(self, scene: Scene, *, sensor: SensorConfig | None = None,
                  frame_buffer: FrameBuffer | None = None, delays=None, dt: float = 0.02, t0: float = 0.0,
                  first_step: int = 0, out: torch.Tensor | None = None, early_termination: bool = True,
-                 rsm: RsmConfig | None = None, rsm_modes=None):
+                 rsm: RsmConfig | None = None, rsm_modes=None, ds_out: torch.Tensor | None = None,
+                 downsample_factor: int = 5):
         if frame_buffer is not None and (delays is None or not dt > 0):
             raise ValueError("frame_buffer needs delays and dt > 0")
         self.scene = scene
@@ -143,6 +161,8 @@ class CapturedStep:
         key = 0
         if rsm is not None:
             _set_rsm(a, scene, rsm, rsm_modes, self._keep)
+        if ds_out is not None:
+            _set_downsample(a, scene, ds_out, downsample_factor)
         if sensor is not None:
             a.flags |= _native.SENSOR
             a.noise_scale = float(sensor.noise_scale)

@@ -361,3 +361,27 @@ def test_fused_rsm_equals_standalone(pkg):
         ref = pkg.rsm_apply(plain, modes, rsm, d_max=scene.d_max_per_camera, step=s)
         assert torch.equal(fused, ref), f"step {s}"
         assert torch.equal(cap.replay(), ref), f"captured step {s}"
+
+
+def test_fused_downsample_equals_standalone(pkg):
+    """render_pipeline(ds_out=...) == downsample_min(obs) (sensor.py:85-100), bitwise, incl. graph replay."""
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    cam = pkg.CameraModel(width=240, height=135, hfov_deg=87.0, vfov_deg=58.0, d_max=6.0,
+                          mount=pkg.look_at_pose([0.0, 0.0, 1.2], [1.5, 0.3, 0.0]))
+    xs = np.linspace(-4, 4, 41)
+    gx, gy = np.meshgrid(xs, xs)
+    gz = 0.2 * np.sin(2 * gx) * np.cos(3 * gy)
+    a = (np.arange(40)[:, None] * 41 + np.arange(40)[None, :]).ravel()
+    faces = np.concatenate([np.column_stack([a, a + 1, a + 42]), np.column_stack([a, a + 42, a + 41])])
+    terrain = pkg.TriMesh(np.column_stack([gx.ravel(), gy.ravel(), gz.ravel()]), faces)
+    scene = pkg.Scene(3, cameras=[cam, cam], terrain=terrain)
+    cfg = pkg.SensorConfig(seed=1)
+    ds = torch.empty((3, 2, 27, 48), device="cuda")
+    obs = pkg.render_pipeline(scene, sensor=cfg, step=2, ds_out=ds)
+    assert torch.equal(ds, pkg.downsample_min(obs, 5))
+    ds2 = torch.empty_like(ds)
+    cap = CapturedStep(scene, sensor=cfg, first_step=2, ds_out=ds2)
+    cap.replay()
+    assert torch.equal(ds2, ds)
+    with pytest.raises(ValueError):
+        pkg.render_pipeline(scene, ds_out=torch.empty((3, 2, 27, 48), device="cuda"), downsample_factor=7)

@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5", "cfg5_1m"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5", "cfg5_1m", "paper"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=None, help="envs per GPU (default: config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -68,7 +68,7 @@ def f32(x):
 
 
 def cfg_envs(name):
-    return {"cfg2": 4096, "cfg3": 4096, "cfg5": 4096, "cfg5_1m": 4096}[name]
+    return {"cfg2": 4096, "cfg3": 4096, "cfg5": 4096, "cfg5_1m": 4096, "paper": 1024}[name]
 
 
 def workload_desc(name):
@@ -79,6 +79,8 @@ def workload_desc(name):
         "cfg5": "4096 envs x 2 cams 160x120, 1300x1300-node rolling terrain (3,373,802 tris, BVH ~270 MB > 2x L2), "
                 "full sensor",
         "cfg5_1m": "4096 envs x 2 cams 160x120, 708x708-node rolling terrain (999,698 tris), full sensor",
+        "paper": "1024 envs x 2 cams 240x135 (paper native res) on the cfg2 tiles, full sensor + latency, "
+                 "fused 5x5 block-min to the 48x27 policy input",
     }[name]
 
 
@@ -291,11 +293,16 @@ def main():
     stream = torch.cuda.current_stream(dev)
     step_id = [0]
 
+    # paper pipeline: the policy consumes the fused 5x5 block minimum of the observation
+    ds = None
+    if args.config == "paper":
+        ds = torch.empty((n, C, H // 5, W // 5), dtype=torch.float32, device=dev)
+
     def step(poses):
         s = step_id[0]
         scene.set_body_poses(poses[0], poses[1], validate=False)
         md.render_pipeline(scene, sensor=sens, step=s, frame_buffer=buf, timestamp=s * dt, delays=delays,
-                           out=out)
+                           out=out, ds_out=ds)
         step_id[0] += 1
 
     # ---- per-ray work counts (untimed, MDRT_COUNT) ----
@@ -332,7 +339,8 @@ def main():
 
     # ---- same step replayed as a captured CUDA graph (device step state) ----
     from paper_2602_03002_b200.pipeline import CapturedStep
-    cap = CapturedStep(scene, sensor=sens, frame_buffer=buf, delays=delays, dt=dt, first_step=step_id[0], out=out)
+    cap = CapturedStep(scene, sensor=sens, frame_buffer=buf, delays=delays, dt=dt, first_step=step_id[0], out=out,
+                       ds_out=ds)
     for i in range(args.warmup):
         scene.body_positions.copy_(pose_dev[i % P][0])
         scene.body_rotations.copy_(pose_dev[i % P][1])

@@ -384,6 +384,13 @@ def config(name: str, num_envs: int | None = None) -> Workload:
         t = tile_field(kinds)
         n = num_envs or (4096 if name == "cfg2" else 32768)
         w = Workload(name, t, g1_links(), torso_cameras(2), n)
+    elif name == "paper":
+        # the paper's training resolution: 1024 envs, 240x135 native depth per camera,
+        # min-pooled 5x to the 48x27 policy input (sensor.py:27-29)
+        kinds = ["slope_pyramid", "stairs_up", "stairs_down"] * 3
+        t = tile_field(kinds)
+        n = num_envs or 1024
+        w = Workload(name, t, g1_links(), torso_cameras(2, width=240, height=135), n)
     elif name == "cfg3":
         t = stepping_stones()
         n = num_envs or 4096

@@ -401,6 +401,9 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
         rp.tiles_x = (ctx->W + kTileW - 1) / kTileW;
         rp.tiles_per_view = rp.tiles_x * ((ctx->H + kTileH - 1) / kTileH);
+        rp.m_tiles_x = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_x));
+        rp.m_tiles_per_view = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_per_view));
+        rp.m_C = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(C));
         rp.early_termination = (a->flags & MDRT_EARLY_TERMINATION) != 0;
         rp.terrain_root = ctx->has_terrain ? ctx->terrain_root : -1;
         rp.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);

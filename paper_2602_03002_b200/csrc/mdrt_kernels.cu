@@ -275,16 +275,24 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
 // ---------------------------------------------------------------------------
 // K1+K2+K3: render + fused sensor epilogue. One warp = one 8x4 tile of a view.
 // ---------------------------------------------------------------------------
+// n / d for 32-bit n with a host-precomputed m = floor((2^32 - 1) / d): the
+// multiply-high estimate is at most one short, fixed by one compare.
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t d, uint32_t m) {
+    uint32_t q = __umulhi(n, m);
+    if (n - q * d >= d) ++q;
+    return q;
+}
+
 template <bool COUNT>
 __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int2* stack) {
-    const uint32_t view = gw / static_cast<uint32_t>(p.tiles_per_view);
+    const uint32_t view = fast_div(gw, static_cast<uint32_t>(p.tiles_per_view), p.m_tiles_per_view);
     const uint32_t tile = gw - view * static_cast<uint32_t>(p.tiles_per_view);
-    const uint32_t ty = tile / static_cast<uint32_t>(p.tiles_x);
+    const uint32_t ty = fast_div(tile, static_cast<uint32_t>(p.tiles_x), p.m_tiles_x);
     const uint32_t tx = tile - ty * static_cast<uint32_t>(p.tiles_x);
     const int px = static_cast<int>(tx) * kTileW + (lane & (kTileW - 1));
     const int py = static_cast<int>(ty) * kTileH + lane / kTileW;
     const bool active = px < p.W && py < p.H;
-    const uint32_t e = view / static_cast<uint32_t>(p.C);
+    const uint32_t e = fast_div(view, static_cast<uint32_t>(p.C), p.m_C);
     const uint32_t c = view - e * static_cast<uint32_t>(p.C);
 
     const ViewRec& V = p.views[view];
@@ -318,6 +326,9 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const int4 tail = *reinterpret_cast<const int4*>(&L.root);  // root | x0,x1 | y0,y1 | pad
         const int x0 = static_cast<int16_t>(tail.y & 0xffff), x1 = tail.y >> 16;
         const int y0 = static_cast<int16_t>(tail.z & 0xffff), y1 = tail.z >> 16;
+        // warp-uniform tile/rect overlap first, per-lane test only when they overlap
+        const int tx0 = static_cast<int>(tx) * kTileW, ty0 = static_cast<int>(ty) * kTileH;
+        if (x1 < tx0 || x0 >= tx0 + kTileW || y1 < ty0 || y0 >= ty0 + kTileH) continue;
         const bool want = active && px >= x0 && px <= x1 && py >= y0 && py <= y1;
         if (!__any_sync(0xffffffffu, want)) continue;
         if (want) {

@@ -60,6 +60,7 @@ struct PrologueParams {
 struct RenderParams {
     int32_t N, C, B, W, H;
     int32_t tiles_x, tiles_per_view;
+    uint32_t m_tiles_x, m_tiles_per_view, m_C;   // fast_div multipliers floor((2^32-1)/d)
     int32_t early_termination;
     int32_t terrain_root;
     const float4* nodes;

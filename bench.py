@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--pose-sets", type=int, default=8)
     ap.add_argument("--gather", action="store_true",
-                    help="N>1: also time the step + NCCL gather of all observations to rank 0")
+                    help="N>1: also time the step + gather of all observations to rank 0 "
+                         "(NCCL, and the fused peer-memory store path)")
     return ap.parse_args()
 
 
@@ -449,7 +450,7 @@ def main():
     d2h_gbs = 5 * d2h / (c0.elapsed_time(c1) * 1e-3) / 1e9
 
     # ---- optional: step + NCCL gather of every rank's observation to rank 0 ----
-    gather_ms = 0.0
+    gather_ms = p2p_ms = 0.0
     if args.gather and world > 1:
         dist.barrier()
         torch.cuda.synchronize()
@@ -464,12 +465,29 @@ def main():
         g1.record(stream)
         torch.cuda.synchronize()
         gather_ms = g0.elapsed_time(g1)
+        # fused gather: the render epilogue stores straight into rank 0's buffers over peer memory
+        start_env = rank * scene.num_envs
+        sink = pdist.PeerFrameSink(scene.frame_shape[1:], world * scene.num_envs, start_env, scene.num_envs,
+                                   dst=0, slots=2, device=dev)
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0.record(stream)
+        for i in range(args.steps):
+            scene.set_body_poses(*pose_dev[i % P], validate=False)
+            md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf,
+                               timestamp=step_id[0] * dt, delays=delays, out=sink.local(i))
+            sink.publish()
+            step_id[0] += 1
+        g1.record(stream)
+        torch.cuda.synchronize()
+        p2p_ms = g0.elapsed_time(g1)
+        sink.close()
 
     # max over ranks
-    tt = torch.tensor([total_ms, e2e_ms, kernel_ms, gather_ms, graph_ms], dtype=torch.float64, device=dev)
+    tt = torch.tensor([total_ms, e2e_ms, kernel_ms, gather_ms, graph_ms, p2p_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms, kernel_ms, gather_ms, graph_ms = tt.tolist()
+    total_ms, e2e_ms, kernel_ms, gather_ms, graph_ms, p2p_ms = tt.tolist()
 
     if rank == 0:
         all_rays = rays_per_step * world * args.steps
@@ -540,7 +558,10 @@ def main():
                       "how": "CapturedStep replay (advance+prologue+render CUDA graph, device step state), "
                              "device pose copy + L2 flush between steps as for value"},
             "gather": ({"value": all_rays / (gather_ms * 1e-3), "unit": "rays/s",
-                        "how": "step + NCCL P2P gather of all observations to rank 0, no L2 flush"}
+                        "how": "step + NCCL P2P gather of all observations to rank 0, no L2 flush",
+                        "fused_p2p": {"value": all_rays / (p2p_ms * 1e-3), "unit": "rays/s",
+                                      "how": "PeerFrameSink: render epilogue stores into rank 0's IPC-mapped "
+                                             "buffers over NVLink + 1-element NCCL all_reduce per step"}}
                        if gather_ms > 0 else None),
             "clocks": clk,
             "wall_s_timed": wall,

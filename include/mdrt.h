@@ -213,6 +213,21 @@ int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_
  * one float per block into `sink` (device, >= 4096 floats) so loads are live. */
 int mdrt_probe_read(const void *buf, int64_t bytes, int32_t iters, float *sink, void *stream);
 
+/* Fused frame gather over peer memory (the reference
+ * has no multi-GPU path, its closest interface is the caller-allocated `out`
+ * of render_batch, numba_backend.py:222-234). The destination rank allocates
+ * the full (N_total, C, H, W) observation buffer with mdrt_peer_alloc and
+ * publishes the 64-byte CUDA IPC handle; every other rank maps it with
+ * mdrt_peer_open and passes `mapped + env_offset*C*H*W` as mdrt_step_args.out,
+ * so the render epilogue stores its block straight into the destination GPU
+ * over NVLink. Ordering between producers and the consumer is the caller's
+ * (a stream-ordered collective barrier). */
+#define MDRT_IPC_HANDLE_BYTES 64
+int mdrt_peer_alloc(int32_t device, int64_t bytes, void **dptr, uint8_t *handle);
+int mdrt_peer_open(int32_t device, const uint8_t *handle, void **dptr);
+int mdrt_peer_close(void *dptr);  /* unmap a mapping made by mdrt_peer_open */
+int mdrt_peer_free(void *dptr);   /* free a buffer made by mdrt_peer_alloc */
+
 /* Synchronise the context's device (debug/tests). */
 int mdrt_sync(mdrt_ctx *ctx);
 

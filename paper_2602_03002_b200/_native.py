@@ -141,6 +141,10 @@ def lib():
                                               vp, _c_i32p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_double, _c_dp, vp]),
             "mdrt_state_get": (ctypes.c_int, [vp, _c_i64p, _c_dp, _c_i32p, _c_i32p, _c_dp, _c_i32p]),
+            "mdrt_peer_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(vp), ctypes.c_char_p]),
+            "mdrt_peer_open": (ctypes.c_int, [ctypes.c_int32, ctypes.c_char_p, ctypes.POINTER(vp)]),
+            "mdrt_peer_close": (ctypes.c_int, [vp]),
+            "mdrt_peer_free": (ctypes.c_int, [vp]),
             "mdrt_sync": (ctypes.c_int, [vp]),
         }
         for name, (res, args) in sig.items():
@@ -155,7 +159,8 @@ def lib():
 EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_create", "mdrt_destroy",
            "mdrt_add_body", "mdrt_set_terrain", "mdrt_set_cameras", "mdrt_commit", "mdrt_get_stats",
            "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
-           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_sync")
+           "mdrt_downsample_min", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_peer_alloc",
+           "mdrt_peer_open", "mdrt_peer_close", "mdrt_peer_free", "mdrt_sync")
 
 
 def check(rc: int) -> None:

@@ -673,6 +673,49 @@ int mdrt_probe_read(const void* buf, int64_t bytes, int32_t iters, float* sink, 
     });
 }
 
+static_assert(sizeof(cudaIpcMemHandle_t) == MDRT_IPC_HANDLE_BYTES, "IPC handle size");
+
+int mdrt_peer_alloc(int32_t device, int64_t bytes, void** dptr, uint8_t* handle) {
+    return guarded([&] {
+        need(dptr && handle && bytes > 0, "bad peer_alloc arguments");
+        CK(cudaSetDevice(device));
+        void* p = nullptr;
+        CK(cudaMalloc(&p, static_cast<size_t>(bytes)));
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            CK(e);
+        }
+        std::memcpy(handle, &h, sizeof(h));
+        *dptr = p;
+    });
+}
+
+int mdrt_peer_open(int32_t device, const uint8_t* handle, void** dptr) {
+    return guarded([&] {
+        need(dptr && handle, "bad peer_open arguments");
+        CK(cudaSetDevice(device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        CK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int mdrt_peer_close(void* dptr) {
+    return guarded([&] {
+        need(dptr != nullptr, "dptr is NULL");
+        CK(cudaIpcCloseMemHandle(dptr));
+    });
+}
+
+int mdrt_peer_free(void* dptr) {
+    return guarded([&] {
+        need(dptr != nullptr, "dptr is NULL");
+        CK(cudaFree(dptr));
+    });
+}
+
 int mdrt_sync(mdrt_ctx* ctx) {
     return guarded([&] {
         need(ctx != nullptr, "ctx is NULL");

@@ -5,11 +5,16 @@ Environments are independent worlds sharing immutable geometry
 (rng.py:1-12), so the render step shards with no collective: rank r of R owns
 the contiguous slice ``env_slice(total, r, R)``, replicates the BVHs, and
 passes ``env_offset`` to its Scene. The only communication is the optional
-frame gather to a policy rank (``gather_frames``).
+frame gather to a policy rank: ``gather_frames`` (NCCL all_gather / grouped
+P2P, a copy after the step) or ``PeerFrameSink`` (the fused path: each rank's
+render epilogue stores its block straight into the destination rank's buffer
+over peer memory, so the transfer overlaps the traversal tile by tile and no
+gather kernel runs).
 """
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import torch
@@ -84,3 +89,172 @@ def gather_frames(obs: torch.Tensor, dst: int | None = 0, group=None) -> torch.T
         return out
     dist.gather(obs, None, dst=dst, group=group)
     return None
+
+
+# ---------------------------------------------------------------------------
+# Fused gather over peer memory (second mechanism)
+# ---------------------------------------------------------------------------
+
+class _DLDevice(ctypes.Structure):
+    _fields_ = [("device_type", ctypes.c_int32), ("device_id", ctypes.c_int32)]
+
+
+class _DLDataType(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_uint8), ("bits", ctypes.c_uint8), ("lanes", ctypes.c_uint16)]
+
+
+class _DLTensor(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("device", _DLDevice), ("ndim", ctypes.c_int32),
+                ("dtype", _DLDataType), ("shape", ctypes.POINTER(ctypes.c_int64)),
+                ("strides", ctypes.POINTER(ctypes.c_int64)), ("byte_offset", ctypes.c_uint64)]
+
+
+class _DLManagedTensor(ctypes.Structure):
+    pass
+
+
+_DL_DELETER = ctypes.CFUNCTYPE(None, ctypes.POINTER(_DLManagedTensor))
+_DLManagedTensor._fields_ = [("dl_tensor", _DLTensor), ("manager_ctx", ctypes.c_void_p),
+                             ("deleter", _DL_DELETER)]
+_KDL_CPU, _KDL_CUDA = 1, 2
+_noop_deleter = _DL_DELETER(lambda _p: None)
+
+
+def wrap_pointer(ptr: int, shape, device: torch.device, keepalive: list) -> torch.Tensor:
+    """A float32 tensor over raw memory at ``ptr`` that torch places on ``device``.
+
+    Used for peer mappings: torch's own pointer query would attribute an
+    IPC-mapped buffer to the GPU that owns it, but kernels on the local GPU
+    address it through the peer mapping, so the tensor must claim the local
+    device. The DLPack structs are appended to ``keepalive``; the caller keeps
+    that list (and the mapping) alive for the tensor's lifetime.
+    """
+    shape = tuple(int(x) for x in shape)
+    shp = (ctypes.c_int64 * len(shape))(*shape)
+    mt = _DLManagedTensor()
+    mt.dl_tensor.data = ctypes.c_void_p(int(ptr))
+    if device.type == "cuda":
+        mt.dl_tensor.device = _DLDevice(_KDL_CUDA, device.index if device.index is not None else 0)
+    else:
+        mt.dl_tensor.device = _DLDevice(_KDL_CPU, 0)
+    mt.dl_tensor.ndim = len(shape)
+    mt.dl_tensor.dtype = _DLDataType(2, 32, 1)   # float32
+    mt.dl_tensor.shape = shp
+    mt.dl_tensor.strides = None                  # C-contiguous
+    mt.dl_tensor.byte_offset = 0
+    mt.deleter = _noop_deleter
+    keepalive.extend([shp, mt])
+    new_capsule = ctypes.pythonapi.PyCapsule_New
+    new_capsule.restype = ctypes.py_object
+    new_capsule.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p]
+    return torch.utils.dlpack.from_dlpack(new_capsule(ctypes.addressof(mt), b"dltensor", None))
+
+
+def peer_block_offsets(full_envs: int, env_start: int, env_count: int, frame_elems_per_env: int) -> tuple[int, int]:
+    """(byte offset, byte length) of an env block inside the destination buffer."""
+    if not 0 <= env_start <= env_start + env_count <= full_envs:
+        raise ValueError(f"env block [{env_start}, {env_start + env_count}) outside [0, {full_envs})")
+    return 4 * env_start * frame_elems_per_env, 4 * env_count * frame_elems_per_env
+
+
+class PeerFrameSink:
+    """Destination-rank observation buffers that every rank's render writes into directly.
+
+    The destination rank (``dst``) allocates ``slots`` buffers of shape
+    (N_total, C, H, W) with ``mdrt_peer_alloc`` and broadcasts their CUDA IPC
+    handles; the other ranks map them (``mdrt_peer_open``). ``local(k)`` is the
+    tensor to pass as ``render_pipeline(out=...)`` on every rank: this rank's
+    env rows of slot ``k`` (on ``dst`` a plain view of its own buffer, on the
+    others a peer view whose stores travel over NVLink inside the render
+    epilogue). ``full(k)`` (dst only) is the gathered (N_total, C, H, W) batch.
+
+    ``publish()`` makes the stores of the steps enqueued so far visible on
+    ``dst``: with NCCL it is a one-element all_reduce on the current stream
+    (kernel completion on every rank orders their peer stores before the
+    collective finishes; no host sync); with gloo it synchronises the stream
+    and runs a host barrier. Use at least two slots and alternate them so a
+    producer never overwrites a slot the destination is still reading: the
+    consumer must enqueue its use of slot k before the ``publish()`` that
+    follows the step writing slot k+1.
+    """
+
+    def __init__(self, frame_shape_per_env, total_envs: int, env_start: int, env_count: int, *,
+                 dst: int = 0, slots: int = 2, group=None, device: torch.device | None = None):
+        from . import _native
+        self._native = _native
+        self.group = group
+        self.dst = dst
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.per_env = tuple(int(x) for x in frame_shape_per_env)
+        self.total_envs = int(total_envs)
+        self.env_start, self.env_count = int(env_start), int(env_count)
+        elems = 1
+        for x in self.per_env:
+            elems *= x
+        self.elems_per_env = elems
+        self.off, _ = peer_block_offsets(self.total_envs, self.env_start, self.env_count, elems)
+        nbytes = 4 * self.total_envs * elems
+        lib = _native.lib()
+        dev = self.device.index if self.device.index is not None else 0
+        self._owned, self._mapped, self._keep = [], [], []
+        handles = None
+        if self.rank == dst:
+            handles = []
+            for _ in range(slots):
+                p = ctypes.c_void_p()
+                h = ctypes.create_string_buffer(64)
+                _native.check(lib.mdrt_peer_alloc(dev, nbytes, ctypes.byref(p), h))
+                self._owned.append(p.value)
+                handles.append(h.raw)
+        if self.world > 1:
+            box = [handles]
+            dist.broadcast_object_list(box, src=dst, group=group)
+            handles = box[0]
+        bases = list(self._owned)
+        if self.rank != dst:
+            for h in handles:
+                p = ctypes.c_void_p()
+                _native.check(lib.mdrt_peer_open(dev, h, ctypes.byref(p)))
+                self._mapped.append(p.value)
+            bases = list(self._mapped)
+        self._local = [wrap_pointer(b + self.off, (self.env_count,) + self.per_env, self.device, self._keep)
+                       for b in bases]
+        self._full = ([wrap_pointer(b, (self.total_envs,) + self.per_env, self.device, self._keep)
+                       for b in bases] if self.rank == dst else None)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device) if self.world > 1 else None
+
+    @property
+    def slots(self) -> int:
+        return len(self._local)
+
+    def local(self, k: int) -> torch.Tensor:
+        return self._local[k % self.slots]
+
+    def full(self, k: int) -> torch.Tensor:
+        if self._full is None:
+            raise RuntimeError(f"rank {self.rank} is not the destination rank {self.dst}")
+        return self._full[k % self.slots]
+
+    def publish(self) -> None:
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=self.group)
+
+    def close(self) -> None:
+        """Unmap / free the buffers (call on every rank, after the last use)."""
+        lib = self._native.lib()
+        torch.cuda.synchronize(self.device)
+        self._local, self._full = [], None
+        for p in self._mapped:
+            self._native.check(lib.mdrt_peer_close(ctypes.c_void_p(p)))
+        if self.world > 1:
+            dist.barrier(group=self.group)   # every mapping closed before the owner frees
+        for p in self._owned:
+            self._native.check(lib.mdrt_peer_free(ctypes.c_void_p(p)))
+        self._mapped, self._owned, self._keep = [], [], []

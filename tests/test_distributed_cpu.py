@@ -95,3 +95,23 @@ def test_two_rank_gloo_slices_and_gather():
         assert np.array_equal(res[r][3], ref)          # all_gather on every rank
     assert np.array_equal(res[0][4], ref)              # gather to rank 0
     assert res[1][4] is None
+
+
+def test_peer_block_offsets_and_pointer_views():
+    """Host logic of the fused peer-memory gather: block offsets and raw-pointer tensor views."""
+    spans = [pd.env_slice(4096, r, 8) for r in range(8)]
+    per_env = 2 * 48 * 64
+    offs = [pd.peer_block_offsets(4096, s, c, per_env) for s, c in spans]
+    assert offs[0] == (0, 4 * 512 * per_env)
+    for (o0, l0), (o1, _) in zip(offs, offs[1:]):
+        assert o0 + l0 == o1
+    with pytest.raises(ValueError):
+        pd.peer_block_offsets(10, 8, 3, per_env)
+    buf = np.arange(10 * 6, dtype=np.float32)
+    keep = []
+    off, _ = pd.peer_block_offsets(10, 4, 3, 6)
+    view = pd.wrap_pointer(buf.ctypes.data + off, (3, 2, 3), torch.device("cpu"), keep)
+    assert view.shape == (3, 2, 3) and view.is_contiguous()
+    assert np.array_equal(view.numpy().ravel(), buf[24:42])
+    view.fill_(-1.0)
+    assert np.all(buf[24:42] == -1.0) and buf[23] == 23.0 and buf[42] == 42.0

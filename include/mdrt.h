@@ -200,6 +200,11 @@ int mdrt_rsm_apply(const float *in, float *out, int32_t N, int32_t C, int32_t H,
 int mdrt_downsample_min(const float *in, float *out, int64_t planes, int32_t H, int32_t W,
                         int32_t factor, void *stream);
 
+/* depth_to_u8 (frameio.py depth_to_u8, PGM previews): out[i] =
+ * round_half_even(255 * (1 - clip(in[i] / d_max, 0, 1))) in f64. in: 16-byte
+ * aligned device float32; out: 4-byte aligned device uint8. */
+int mdrt_depth_to_u8(const float *in, uint8_t *out, int64_t n, double d_max, void *stream);
+
 /* Host-only BVH check (no device needed): builds the packed tree for one mesh
  * exactly as mdrt_add_body/mdrt_set_terrain do and verifies its invariants
  * (every triangle in exactly one leaf, child boxes enclose their triangles,

@@ -21,6 +21,7 @@ module is the numpy glue that restates the reference's host-side steps
 * ``frame_select``        sensor.py:133-150 (C: orc_frame_select)
 * ``downsample_min``      sensor.py:85-100  (C: orc_downsample_min)
 * ``rsm_*``               perception.py:150-202 (C: orc_rsm_apply; modes via categorical)
+* ``depth_to_u8``/``mdpt_bytes`` frameio.py:21-38, 81-86 (numpy)
 
 Pinned against the live reference by tests/golden/make_golden.py.
 """
@@ -416,6 +417,19 @@ def downsample_min(depth, factor):
     out = np.empty(depth.shape[:-2] + (h // factor, w // factor), np.float32)
     lib().orc_downsample_min(_p(depth, _fp), planes, h, w, factor, _p(out, _fp))
     return out
+
+
+def depth_to_u8(depth, d_max):
+    """frameio.py:81-86: f64 ratio, clip to [0, 1], round-half-even of 255 * (1 - frac)."""
+    frac = np.clip(np.asarray(depth, np.float64) / float(d_max), 0.0, 1.0)
+    return np.rint(255.0 * (1.0 - frac)).astype(np.uint8)
+
+
+def mdpt_bytes(depth):
+    """frameio.py:21-38: '<4sHIIII' header (MDPT, 1, N, C, H, W) + little-endian float32 payload."""
+    import struct
+    a = np.ascontiguousarray(depth, np.float32)
+    return struct.pack("<4sHIIII", b"MDPT", 1, *a.shape) + a.astype("<f4").tobytes()
 
 
 def categorical(key, probs, *counters):

@@ -22,6 +22,8 @@ from .sensor import (SensorConfig, CameraRandomization, FrameBuffer, apply_noise
 from .perception import (RsmConfig, RSM_MODES, DEFAULT_RSM_PROBS, rsm_sample_modes, rsm_mask_columns,
                          rsm_apply)
 from .pipeline import CapturedStep, render_pipeline
+from .frameio import (FormatError, FrameWriter, write_frames, read_frames, write_grid, read_grid, depth_to_u8,
+                      write_pgm, read_pgm)
 
 __version__ = "0.1.0"
 
@@ -36,5 +38,6 @@ __all__ = [
     "SensorConfig", "CameraRandomization", "FrameBuffer", "apply_noise_dropout", "downsample_min",
     "sample_latencies", "sample_camera_offsets", "randomize_scene_cameras", "randomized_camera",
     "RsmConfig", "RSM_MODES", "DEFAULT_RSM_PROBS", "rsm_sample_modes", "rsm_mask_columns", "rsm_apply",
-    "render_pipeline", "CapturedStep", "__version__",
+    "render_pipeline", "CapturedStep", "FormatError", "FrameWriter", "write_frames", "read_frames",
+    "write_grid", "read_grid", "depth_to_u8", "write_pgm", "read_pgm", "__version__",
 ]

@@ -611,6 +611,18 @@ int mdrt_downsample_min(const float* in, float* out, int64_t planes, int32_t H, 
     });
 }
 
+int mdrt_depth_to_u8(const float* in, uint8_t* out, int64_t n, double d_max, void* stream) {
+    return guarded([&] {
+        need(in && out, "NULL argument");
+        need(d_max > 0.0, "d_max must be positive");
+        need(reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 4 == 0,
+             "depth_to_u8 needs 16-byte aligned input and 4-byte aligned output");
+        if (n <= 0) return;
+        launch_depth_u8(in, out, n, d_max, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
 int mdrt_bvh_check(const double* verts, int64_t nv, const int64_t* faces, int64_t nf, int64_t info[4]) {
     return guarded([&] {
         need(verts && faces && info, "NULL argument");

@@ -525,6 +525,31 @@ static __global__ void downsample_kernel(DownsampleParams p) {
     p.out[i] = mn;
 }
 
+// depth_to_u8 (frameio.py depth_to_u8): round(255 * (1 - clip(d / d_max, 0, 1))) in f64,
+// round-half-even like np.round; 4 pixels per thread (16 B in, 4 B out).
+__device__ __forceinline__ uint8_t gray_of(float d, double dmax) {
+    double f = __ddiv_rn(static_cast<double>(d), dmax);
+    f = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+    return static_cast<uint8_t>(rint(__dmul_rn(255.0, __dadd_rn(1.0, -f))));
+}
+
+static __global__ void depth_u8_kernel(const float* __restrict__ in, uint8_t* __restrict__ out, int64_t n,
+                                       double dmax) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = q * 4;
+    if (i + 4 <= n) {
+        const float4 v = *reinterpret_cast<const float4*>(in + i);
+        uchar4 o;
+        o.x = gray_of(v.x, dmax);
+        o.y = gray_of(v.y, dmax);
+        o.z = gray_of(v.z, dmax);
+        o.w = gray_of(v.w, dmax);
+        *reinterpret_cast<uchar4*>(out + i) = o;
+    } else {
+        for (int64_t k = i; k < n; ++k) out[k] = gray_of(in[k], dmax);
+    }
+}
+
 // read-bandwidth probe: grid-stride 16 B loads, one partial sum per block
 static __global__ void __launch_bounds__(256) probe_read_kernel(const float4* __restrict__ buf, int64_t n16,
                                                                 int iters, float* sink) {
@@ -639,6 +664,10 @@ void launch_rsm(const RsmParams& p, int64_t total, cudaStream_t s) {
 
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s) {
     downsample_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);
+}
+
+void launch_depth_u8(const float* in, uint8_t* out, int64_t n, double dmax, cudaStream_t s) {
+    depth_u8_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(in, out, n, dmax);
 }
 
 }  // namespace mdrt

@@ -143,6 +143,7 @@ void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s);
 void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s);
 void launch_select(const SelectParams& p, int64_t n, cudaStream_t s);
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s);
+void launch_depth_u8(const float* in, uint8_t* out, int64_t n, double dmax, cudaStream_t s);
 void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, cudaStream_t s);
 void launch_advance(StepState* st, cudaStream_t s);
 void launch_rsm(const RsmParams& p, int64_t total, cudaStream_t s);

@@ -133,9 +133,31 @@ def random_case(md, rng, num_envs=2, num_cams=2, width=32, height=24, num_bodies
     return case_from_reference(md, bodies, (verts, faces), cams, pos, rot, rand=rand)
 
 
+def make_frameio(md):
+    """MDPT / PGM bytes and depth_to_u8 vectors from the reference frameio.py."""
+    g = np.random.default_rng(5)
+    depth = g.uniform(-0.5, 11.0, size=(3, 2, 27, 48)).astype(np.float32)
+    depth[0, 0, 0, :8] = np.float32([0.0, 10.0, 5.0, 2.5, 7.5, 1.25, 8.75, 3.75])   # exact half-way grays
+    fio = {"depth": depth}
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "f.mdpt")
+        md.write_frames(path, depth)
+        fio["mdpt_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        md.write_grid(path, depth[1, 1].astype(np.float64))
+        fio["grid_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        for k, dmax in enumerate((10.0, 8.0, 0.7)):
+            fio[f"u8_{k}"] = md.depth_to_u8(depth, dmax)
+        fio["u8_dmax"] = np.array([10.0, 8.0, 0.7])
+        pgm = os.path.join(tmp, "p.pgm")
+        md.write_pgm(pgm, fio["u8_0"][0, 1])
+        fio["pgm_bytes"] = np.frombuffer(open(pgm, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "frameio.npz"), **fio)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=os.environ.get("MULTIDEPTH_REF", "/root/reference/pkg/src"))
+    ap.add_argument("--only", choices=["frameio"], default=None, help="regenerate one fixture group")
     args = ap.parse_args()
     os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_cache_golden"))
     sys.dont_write_bytecode = True
@@ -145,6 +167,10 @@ def main():
     from multidepth import rng as mrng
     from paper_2602_03002_b200 import synth
 
+    make_frameio(md)
+    if args.only == "frameio":
+        print("done")
+        return
     out = {}
     rng = np.random.default_rng(20261018)
     for k in range(6):

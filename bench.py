@@ -159,11 +159,13 @@ def run_cpu_sample(orc, w, sc, n_sample, step, threads, buf_state, delays, cfg):
     sl = slice(0, n_sample)
     bp, bq = w.poses(step, sl)
     bp, bq = f32(bp).astype(np.float64), f32(bq).astype(np.float64)
+    t0 = time.perf_counter()
     depth = sc.render(bp, bq, threads=threads)
+    buf_state[2].append(time.perf_counter() - t0)
     dmax = np.array([c["d_max"] for c in sc.cameras])
     noisy = orc.apply_noise_dropout(depth, noise_scale=cfg.noise_scale, dropout_p=cfg.dropout_p, seed=cfg.seed,
                                     d_max=dmax, step=step, threads=threads)
-    times, frames = buf_state
+    times, frames = buf_state[0], buf_state[1]
     times.append(step * 0.02)
     frames.append(noisy)
     if len(times) > 8:
@@ -183,14 +185,15 @@ def cpu_measure(name, steps, warmup, seconds_target, threads):
     delays = sensor.sample_latencies(sensor.SensorConfig(max_delay=0.1, seed=3), w.num_envs)
     rays_per_env = len(w.cameras) * w.cameras[0].width * w.cameras[0].height
     # size the sample so each step costs ~seconds_target / steps
-    state = ([], [])
+    state = ([], [], [])
     t0 = time.perf_counter()
     run_cpu_sample(orc, w, sc, probe_n, 0, threads, state, delays, cfg)
     per_env = (time.perf_counter() - t0) / probe_n
     n_sample = int(max(8, min(w.num_envs, seconds_target / max(steps, 1) / max(per_env, 1e-6))))
-    state = ([], [])
+    state = ([], [], [])
     for s in range(warmup):
         run_cpu_sample(orc, w, sc, n_sample, s, threads, state, delays, cfg)
+    state[2].clear()
     times = []
     for s in range(steps):
         t0 = time.perf_counter()
@@ -200,7 +203,9 @@ def cpu_measure(name, steps, warmup, seconds_target, threads):
     value = rays * len(times) / sum(times)
     desc = (f"{n_sample} of {w.num_envs} envs x {len(w.cameras)} cams x {w.cameras[0].width}x"
             f"{w.cameras[0].height} per step (render + noise/dropout + latency), {len(times)} steps")
-    return value, desc, times
+    split = {"render_plus_sensor_mean": value, "render_plus_sensor_best": rays / min(times),
+             "render_only_mean": rays * len(state[2]) / sum(state[2]), "render_only_best": rays / min(state[2])}
+    return value, desc, times, split
 
 
 def cpu_info():
@@ -221,7 +226,7 @@ def reference_arm(args):
         return 0
     from oracle import oracle as orc
     threads = orc.max_threads()
-    value, desc, _ = cpu_measure(args.config, args.steps, args.warmup, args.cpu_seconds * 3, threads)
+    value, desc, _, split = cpu_measure(args.config, args.steps, args.warmup, args.cpu_seconds * 3, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
@@ -229,7 +234,7 @@ def reference_arm(args):
         "config": {"workload": workload_desc(args.config), "impl_detail": "oracle/oracle.c (C restatement of "
                    "multidepth numba_backend._render_kernel + sensor + FrameBuffer), OpenMP"},
         "cpu_baseline": {"value": value, "unit": "rays/s", "cores": threads, "kind": "port", "sample": desc,
-                         "cpu": cpu_info()},
+                         "cpu": cpu_info(), "split": split},
         "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -516,8 +521,9 @@ def main():
         if not args.no_cpu_baseline and world == 1:
             from oracle import oracle as orc
             th = orc.max_threads()
-            cv, cdesc, _ = cpu_measure(args.config, 3, 1, args.cpu_seconds, th)
-            cpu = {"value": cv, "unit": "rays/s", "cores": th, "kind": "port", "sample": cdesc, "cpu": cpu_info()}
+            cv, cdesc, _, split = cpu_measure(args.config, 3, 1, args.cpu_seconds, th)
+            cpu = {"value": cv, "unit": "rays/s", "cores": th, "kind": "port", "sample": cdesc, "cpu": cpu_info(),
+                   "split": split}
         line = {
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

@@ -14,6 +14,11 @@ namespace mdrt {
 
 constexpr int kStack = 24;          // == kMaxDepth of the builder
 constexpr int kBlock = 128;         // threads per render block (4 warps, 4 tiles)
+#ifdef MDRT_SHARED_STACK
+constexpr int kStackStride = kBlock;  // this thread's column of a block-wide shared stack
+#else
+constexpr int kStackStride = 1;       // per-thread stack in local memory (L1-cached)
+#endif
 #ifndef MDRT_TILE_W
 #define MDRT_TILE_W 8
 #endif
@@ -199,7 +204,7 @@ struct Traversal {
 
     __device__ __forceinline__ int32_t pop() {
         while (top != bottom) {
-            top -= kBlock;
+            top -= kStackStride;
             const int2 e = *top;
             if (__int_as_float(e.y) <= best) return e.x;
         }
@@ -263,7 +268,7 @@ struct Traversal {
             if (h0 && h1) {
                 const bool swap = c1min < c0min;
                 *top = make_int2(swap ? rf.x : rf.y, __float_as_int(swap ? c0min : c1min));
-                top += kBlock;
+                top += kStackStride;
                 ref = swap ? rf.y : rf.x;
             } else if (h0 || h1) {
                 ref = h0 ? rf.x : rf.y;

@@ -13,7 +13,10 @@
 namespace mdrt {
 
 constexpr int kStack = 24;          // == kMaxDepth of the builder
-constexpr int kBlock = 128;         // threads per render block (4 warps, 4 tiles)
+#ifndef MDRT_BLOCK
+#define MDRT_BLOCK 128
+#endif
+constexpr int kBlock = MDRT_BLOCK;  // threads per render block (4 warps, 4 tiles)
 #ifdef MDRT_SHARED_STACK
 constexpr int kStackStride = kBlock;  // this thread's column of a block-wide shared stack
 #else

@@ -283,6 +283,12 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t d, uint32_t m)
     return q;
 }
 
+#ifdef MDRT_PLAIN_STORES
+__device__ __forceinline__ void st_stream(float* p, float v) { *p = v; }
+#else
+__device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
+#endif
+
 template <bool COUNT>
 __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int2* stack) {
     const uint32_t view = fast_div(gw, static_cast<uint32_t>(p.tiles_per_view), p.m_tiles_per_view);
@@ -391,13 +397,15 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     }
     if (active) {
         const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
-        if (p.out_clean) p.out_clean[o] = z;
+        if (p.out_clean) st_stream(p.out_clean + o, z);
         if (p.ring) {
+            // ring traffic streams past L1/L2 (evict-first) so it does not
+            // displace BVH records; a zero-lag read is the value just written
             const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
             const int wslot = p.state ? p.state->write_slot : p.write_slot;
-            p.ring[static_cast<int64_t>(wslot) * frame + o] = val;
+            st_stream(p.ring + static_cast<int64_t>(wslot) * frame + o, val);
             const int rs = V.read_slot;
-            if (rs >= 0) val = p.ring[static_cast<int64_t>(rs) * frame + o];
+            if (rs >= 0 && rs != wslot) val = __ldcs(p.ring + static_cast<int64_t>(rs) * frame + o);
         }
         if (p.rsm) {
             // random side masking of the observation (perception.py:183-202)
@@ -408,7 +416,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
                 val = static_cast<float>(__dadd_rn(p.rsm_low, __dmul_rn(p.rsm_high[c] - p.rsm_low, unit53(h))));
             }
         }
-        if (p.out) p.out[o] = val;
+        if (p.out) st_stream(p.out + o, val);
     }
     if (p.ds_out) {
         // block-minimum downsample of the observation (sensor.py:85-100): lanes of

@@ -383,8 +383,9 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         }
         pp.views = ctx->views.ptr;
         pp.links = ctx->links.ptr;
-        ctx->tile_counter.reserve(1);
+        ctx->tile_counter.reserve(kTileCounters);
         pp.reset_counter = ctx->tile_counter.ptr;
+        pp.reset_count = kTileCounters;
         const bool only_pro = (a->flags & MDRT_PHASE_PROLOGUE) && !(a->flags & MDRT_PHASE_TRACE);
         const bool only_trace = (a->flags & MDRT_PHASE_TRACE) && !(a->flags & MDRT_PHASE_PROLOGUE);
         if (dstate && !only_trace) {
@@ -436,12 +437,15 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
             CK(cudaMemsetAsync(a->ds_out, 0x7f, sizeof(float) * nviews * rp.ds_w * rp.ds_h, s));
         rp.rsm_low = a->rsm_fill_low;
         for (int c = 0; c < C; ++c) rp.rsm_high[c] = a->rsm_fill_high ? a->rsm_fill_high[c] : ctx->rigs[c].d_max;
-        ctx->tile_counter.reserve(1);
+        ctx->tile_counter.reserve(kTileCounters);
         rp.tile_counter = ctx->tile_counter.ptr;
         const int64_t warps = static_cast<int64_t>(nviews) * rp.tiles_per_view;
         need(warps < (int64_t(1) << 31), "launch too large");
-        if (only_trace) CK(cudaMemsetAsync(rp.tile_counter, 0, sizeof(unsigned int), s));  // prologue not run
-        launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, s);
+        if (only_trace)   // prologue not run
+            CK(cudaMemsetAsync(rp.tile_counter, 0, sizeof(unsigned int) * kTileCounters, s));
+        const int64_t geometry_bytes = static_cast<int64_t>(ctx->nodes.cap * sizeof(PackedNode) +
+                                                            ctx->tris.cap * sizeof(PackedTri));
+        launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, geometry_bytes, s);
         CK(cudaGetLastError());
     });
 }
@@ -474,7 +478,7 @@ int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, uint64_
         const size_t nviews = static_cast<size_t>(num_envs) * ctx->C;
         ctx->views.reserve(nviews);
         ctx->links.reserve(std::max<size_t>(1, nviews * std::max<size_t>(ctx->bodies.size(), 1)));
-        ctx->tile_counter.reserve(1);
+        ctx->tile_counter.reserve(kTileCounters);
         CK(cudaMemcpy(ctx->state.ptr, &st, sizeof(st), cudaMemcpyHostToDevice));
     });
 }

@@ -10,6 +10,8 @@ namespace mdrt {
 // Device-resident per-step bookkeeping for graph replay (MDRT_DEVICE_STATE):
 // advance_kernel produces step k's RNG prefixes, timestamp and latency-ring
 // push exactly as the host path would (FrameBuffer._reserve semantics).
+constexpr int kTileCounters = 1025;   // <= 1024 SM chunks + the shared pool
+
 struct StepState {
     unsigned long long key;       // rng.stream_key(seed, "sensor")
     unsigned long long hu_step;   // absorb(absorb(key, 0), k)
@@ -49,7 +51,8 @@ struct PrologueParams {
     int32_t* read_slot_out;
     ViewRec* views;
     LinkRec* links;
-    unsigned int* reset_counter;  // render kernel's tile counter, zeroed here (prologue runs first)
+    unsigned int* reset_counter;  // render kernel's tile counters, zeroed here (prologue runs first)
+    int32_t reset_count;          // number of counters to zero
     const StepState* state;       // non-null: step/ring/RNG fields come from device state
     // random side masking (perception.py:169-202)
     const int32_t* rsm_modes;     // (N, C) mode per view or NULL
@@ -79,7 +82,10 @@ struct RenderParams {
     float* out_clean;
     float* out;
     unsigned long long* counters;
-    unsigned int* tile_counter;   // persistent-warp work counter (zeroed per launch)
+    unsigned int* tile_counter;   // persistent-warp work counters (zeroed per launch): one per
+                                  // SM chunk, then the shared pool (kTileCounters entries)
+    int32_t chunks;               // SM-local chunks (0: one shared counter only)
+    uint32_t local_tiles;         // tiles [0, local_tiles) are split into `chunks` chunks
     int32_t count_detail;         // counters has 4 slots: + link node fetches, link traversals
     const StepState* state;       // non-null: ring write slot comes from device state
     unsigned int* ds_out;         // (N, C, H/f, W/f) block-min of the observation (float bits) or NULL
@@ -138,7 +144,9 @@ struct DownsampleParams {
 
 // Host-side launchers (defined next to the kernels so templates instantiate there).
 void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s);
-void launch_render(const RenderParams& p, int64_t warps, bool count, cudaStream_t s);
+// geometry_bytes: BVH node + triangle bytes; above the L2 size the tiles are
+// scheduled SM-locally (render_kernel) so node reuse comes from L1.
+void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geometry_bytes, cudaStream_t s);
 void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s);
 void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s);
 void launch_select(const SelectParams& p, int64_t n, cudaStream_t s);

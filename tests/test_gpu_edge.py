@@ -92,3 +92,36 @@ def test_many_cameras_parented_to_moving_link(pkg, oracle):
                                     mount=mount, parent_body=c % 6))
     # mounts rounded to what crosses the ABI (f64 mounts, f32 poses)
     _check(pkg, oracle, bodies, terrain, cams, pos, rot, 2, max_bad=2)
+
+
+_SCHED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[2])
+import paper_2602_03002_b200 as md
+from paper_2602_03002_b200 import synth
+w = synth.config("cfg2", 512)
+f32 = lambda x: np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+bodies = [(nm, md.TriMesh(f32(m.vertices), m.faces, frame="body-local")) for nm, m in w.bodies]
+scene = md.Scene(w.num_envs, bodies=bodies, cameras=w.cameras,
+                 terrain=md.TriMesh(f32(w.terrain.mesh.vertices), w.terrain.mesh.faces))
+p, q = w.poses(1)
+scene.set_body_poses(p, q)
+out = md.render_pipeline(scene, sensor=md.SensorConfig(seed=2), step=1)
+np.save(sys.argv[1], out.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("frac", ["0.5", "0.95", "1.0"])
+def test_sm_local_tile_schedule_is_bitwise_identical(tmp_path, frac):
+    """The SM-local tile schedule (chunks + pool + stealing) renders every tile exactly once."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for f in ("0", frac):
+        path = tmp_path / f"o{f}.npy"
+        env = dict(os.environ, MDRT_LOCAL_FRAC=f)
+        subprocess.run([sys.executable, "-c", _SCHED_SCRIPT, str(path), root], check=True, env=env, timeout=300)
+        outs[f] = np.load(path)
+    assert np.array_equal(outs["0"], outs[frac])

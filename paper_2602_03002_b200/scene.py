@@ -166,7 +166,9 @@ class Scene:
 
         Quaternions are normalised on the device (in f64) by the prologue
         kernel, so any nonzero norm is accepted as in the reference.
-        Pinned host tensors are copied asynchronously on the current stream.
+        Pinned host tensors are uploaded asynchronously on the scene's upload
+        stream (overlapping kernels already queued), ordered before the next
+        render on the current stream.
         ``validate=False`` skips the finite/zero-norm checks (for CUDA inputs
         they need a device->host read).
         """
@@ -190,8 +192,41 @@ class Scene:
                 raise ValueError("poses must be finite")
             if bool(small.item()):
                 raise ValueError("zero quaternion in body rotations")
+        if pos.device.type == "cpu" and pos.is_pinned() and rot.is_pinned() and pos.numel():
+            self._upload_poses(pos, rot)
+            return
         for dst, src in ((self.body_positions, pos), (self.body_rotations, rot)):
             dst.copy_(src, non_blocking=src.device.type == "cpu" and src.is_pinned())
+
+    def _upload_poses(self, pos: torch.Tensor, rot: torch.Tensor) -> None:
+        """Pinned host poses: H2D on the scene's upload stream into one of two
+        staging buffers, so the PCIe transfer overlaps the previous step's
+        kernels; the current stream then waits for it and copies staging ->
+        body_positions/body_rotations device-to-device (fixed pointers, so
+        captured graphs keep working). The caller must not modify ``pos``/``rot``
+        until that copy ran (as for any non_blocking copy)."""
+        if not hasattr(self, "_up_stream"):
+            self._up_stream = torch.cuda.Stream(self.device)
+            self._up_pos = [torch.empty_like(self.body_positions) for _ in range(2)]
+            self._up_rot = [torch.empty_like(self.body_rotations) for _ in range(2)]
+            self._up_free = [None, None]
+            self._up_slot = 0
+        j = self._up_slot = self._up_slot ^ 1
+        cur = torch.cuda.current_stream(self.device)
+        up = self._up_stream
+        if self._up_free[j] is not None:
+            up.wait_event(self._up_free[j])        # previous D2D copy out of slot j was enqueued
+        with torch.cuda.stream(up):
+            self._up_pos[j].copy_(pos, non_blocking=True)
+            self._up_rot[j].copy_(rot, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(up)
+        cur.wait_event(ready)
+        self.body_positions.copy_(self._up_pos[j])
+        self.body_rotations.copy_(self._up_rot[j])
+        free = torch.cuda.Event()
+        free.record(cur)
+        self._up_free[j] = free
 
     def body_pose(self, env: int, body: int) -> RigidPose:
         return RigidPose(self.body_positions[env, body].double().cpu().numpy(),

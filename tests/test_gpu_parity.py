@@ -333,6 +333,37 @@ def test_captured_step_matches_eager(pkg):
     assert st["next_step"] == 10 and st["times"] == fb_e._times and st["order"] == fb_e._slots
 
 
+def test_pinned_pose_upload_overlaps_and_matches(pkg):
+    """Pinned host poses go through the scene's upload stream + staging double buffer;
+    results equal the synchronous path, also when the host reuses two pinned buffers
+    and when a captured graph reads the poses."""
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    case = casefile.load(os.path.join(GOLDEN, "render_cfg2_slice.npz"))
+    s_pin, s_ref, s_graph = (casefile.build_scene(case, pkg) for _ in range(3))
+    cfg = pkg.SensorConfig(seed=3)
+    cap = CapturedStep(s_graph, sensor=cfg, first_step=0)
+    rng = np.random.default_rng(4)
+    host = [(torch.empty(case["body_pos"].shape, dtype=torch.float32).pin_memory(),
+             torch.empty(case["body_rot"].shape, dtype=torch.float32).pin_memory()) for _ in range(2)]
+    outs = [torch.empty(s_pin.frame_shape, device="cuda") for _ in range(2)]
+    got, want = [], []
+    for k in range(6):
+        pos = (case["body_pos"] + rng.normal(0, 0.02, case["body_pos"].shape)).astype(np.float32)
+        hp, hq = host[k % 2]
+        if k >= 2:
+            torch.cuda.current_stream().synchronize()   # host buffer k%2 was consumed two steps ago
+        hp.copy_(torch.from_numpy(pos))
+        hq.copy_(torch.from_numpy(case["body_rot"].astype(np.float32)))
+        s_pin.set_body_poses(hp, hq, validate=False)
+        got.append(pkg.render_pipeline(s_pin, sensor=cfg, step=k, out=outs[k % 2]).clone())
+        s_ref.set_body_poses(pos, case["body_rot"])
+        want.append(pkg.render_pipeline(s_ref, sensor=cfg, step=k))
+        s_graph.set_body_poses(hp, hq, validate=False)
+        assert torch.equal(cap.replay(), want[-1]), f"graph step {k}"
+    for k in range(6):
+        assert torch.equal(got[k], want[k]), f"step {k}"
+
+
 def test_rsm_matches_reference(pkg, sens):
     """Random side masking (perception.py:150-202): modes and fills bit-exact vs reference goldens."""
     cfg = pkg.RsmConfig(seed=3)

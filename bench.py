@@ -104,6 +104,11 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(gpu_index),
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a few hundred ms to start: wait for its first sample so
+            # short timed regions are still covered
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 3.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 

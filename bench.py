@@ -263,10 +263,18 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         args.gpus = world if world > 1 else args.gpus
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # MDRT_BENCH_SHARE_GPU=1 (control-flow check only, never a measurement): ranks share
+    # the visible GPUs round-robin and talk over gloo, so the N>1 code path can be
+    # exercised on a one-GPU box; kernels of different ranks never wait on each other.
+    share = os.environ.get("MDRT_BENCH_SHARE_GPU") == "1"
+    gpu = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     n = args.envs or cfg_envs(args.config)
     total_envs = n * world

@@ -105,7 +105,13 @@ def _p(a, ct):
 
 
 def max_threads() -> int:
-    return int(lib().orc_max_threads())
+    """All host cores this process may run on (launchers such as torchrun set
+    OMP_NUM_THREADS=1, which would make the CPU baseline single-threaded)."""
+    try:
+        import os
+        return max(len(os.sched_getaffinity(0)), 1)
+    except (AttributeError, OSError):
+        return int(lib().orc_max_threads())
 
 
 # ---------------------------------------------------------------------------

@@ -56,6 +56,10 @@ def gather_frames(obs: torch.Tensor, dst: int | None = 0, group=None) -> torch.T
     """
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return obs
+    if dist.get_backend(group) == "gloo" and obs.device.type == "cuda":
+        # gloo collectives are host-side: stage through the CPU
+        res = gather_frames(obs.cpu(), dst, group)
+        return None if res is None else res.to(obs.device)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     obs = obs.contiguous()

@@ -205,6 +205,10 @@ struct Traversal {
         top = bottom = stack;
     }
 
+    __device__ __forceinline__ void push(int2 e) {
+        *top = e;
+        top += kStackStride;
+    }
     __device__ __forceinline__ int32_t pop() {
         while (top != bottom) {
             top -= kStackStride;
@@ -270,8 +274,7 @@ struct Traversal {
             const bool h1 = c1min <= c1max;
             if (h0 && h1) {
                 const bool swap = c1min < c0min;
-                *top = make_int2(swap ? rf.x : rf.y, __float_as_int(swap ? c0min : c1min));
-                top += kStackStride;
+                push(make_int2(swap ? rf.x : rf.y, __float_as_int(swap ? c0min : c1min)));
                 ref = swap ? rf.y : rf.x;
             } else if (h0 || h1) {
                 ref = h0 ? rf.x : rf.y;

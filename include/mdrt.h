@@ -44,6 +44,7 @@ extern "C" {
 #define MDRT_PHASE_TRACE 0x40      /* launch only the traversal kernel (uses the last prologue's records)  */
 #define MDRT_COUNT_DETAIL 0x80     /* with MDRT_COUNT: counters has 4 slots (+ link node fetches, link traversals) */
 #define MDRT_RSM 0x200             /* random side masking of the output (perception.py:169-202)             */
+#define MDRT_ROT_XYZW 0x400       /* link_states quaternions are stored x, y, z, w (simulator order)     */
 #define MDRT_DEVICE_STATE 0x100    /* step, timestamp, RNG prefix and ring push come from the context's device
                                       state (mdrt_state_set), advanced on the device at the start of the call:
                                       the call is then CUDA-graph capturable and replayable with no host args */
@@ -121,6 +122,18 @@ typedef struct {
     /* fused downsample_min (sensor.py:85-100) of the final output */
     float *ds_out;             /* (N,C,H/f,W/f) block minimum, or NULL; `out` may then be NULL */
     int32_t ds_factor;         /* f; H and W must be divisible by f                          */
+
+    /* zero-copy pose source (device-side pose ingestion from a
+     * simulator's link-state tensor). When non-NULL it replaces body_pos/body_rot:
+     * body b of env e reads the record link_states + (e * env_stride + link_map[b]) *
+     * record_stride floats, position at +pos_offset, quaternion at +rot_offset (wxyz,
+     * or xyzw with MDRT_ROT_XYZW). */
+    const float *link_states;
+    int64_t env_stride;        /* records per env                                        */
+    int32_t record_stride;     /* floats per record (e.g. 13: pos, quat, lin vel, ang vel) */
+    int32_t pos_offset;
+    int32_t rot_offset;
+    const int32_t *link_map;   /* (B,) device: record index of each body within its env  */
 } mdrt_step_args;
 
 /* ---- library ---------------------------------------------------------- */

@@ -30,6 +30,7 @@ PHASE_TRACE = 0x40
 COUNT_DETAIL = 0x80
 DEVICE_STATE = 0x100
 RSM = 0x200
+ROT_XYZW = 0x400
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -86,6 +87,12 @@ class StepArgs(ctypes.Structure):
         ("rsm_fill_high", _c_dp),
         ("ds_out", ctypes.c_void_p),
         ("ds_factor", ctypes.c_int32),
+        ("link_states", ctypes.c_void_p),
+        ("env_stride", ctypes.c_int64),
+        ("record_stride", ctypes.c_int32),
+        ("pos_offset", ctypes.c_int32),
+        ("rot_offset", ctypes.c_int32),
+        ("link_map", ctypes.c_void_p),
     ]
 
 

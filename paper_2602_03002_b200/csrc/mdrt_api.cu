@@ -306,7 +306,14 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         }
         const bool seam = a->cam_pos != nullptr;
         need(!seam || a->cam_rot != nullptr, "cam_rot is NULL while cam_pos is set");
-        need(B == 0 || (a->body_pos && a->body_rot), "body poses are NULL");
+        need(B == 0 || (a->body_pos && a->body_rot) || a->link_states, "body poses are NULL");
+        if (a->link_states) {
+            need(a->link_map != nullptr, "link_map is NULL while link_states is set");
+            need(a->record_stride >= 7 && a->env_stride >= 1, "bad link_states strides");
+            need(a->pos_offset >= 0 && a->pos_offset + 3 <= a->record_stride && a->rot_offset >= 0 &&
+                     a->rot_offset + 4 <= a->record_stride,
+                 "link_states offsets outside the record");
+        }
         need(!(a->cam_off_pos || a->cam_off_rot) || (a->cam_off_pos && a->cam_off_rot),
              "cam_off_pos and cam_off_rot must be given together");
         need(!a->ray_dirs || a->ray_scale, "ray_scale is NULL while ray_dirs is set");
@@ -342,6 +349,13 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         pp.bodies = ctx->body_info.ptr;
         pp.body_pos = a->body_pos;
         pp.body_rot = a->body_rot;
+        pp.link_states = a->link_states;
+        pp.env_stride = a->env_stride;
+        pp.record_stride = a->record_stride;
+        pp.pos_offset = a->pos_offset;
+        pp.rot_offset = a->rot_offset;
+        pp.rot_xyzw = (a->flags & MDRT_ROT_XYZW) != 0;
+        pp.link_map = a->link_map;
         pp.off_pos = seam ? nullptr : a->cam_off_pos;
         pp.off_rot = seam ? nullptr : a->cam_off_rot;
         pp.fov_delta = a->ray_dirs ? nullptr : a->fov_delta;

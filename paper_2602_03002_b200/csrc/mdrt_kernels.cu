@@ -56,6 +56,27 @@ __device__ __forceinline__ void qmat(Q q, double m[9]) {
     m[6] = 2 * (x * z - w * y);     m[7] = 2 * (y * z + w * x);     m[8] = 1 - 2 * (x * x + y * y);
 }
 
+// Pose of body b in env e: the scene's (N,B,3)/(N,B,4) buffers, or a record of
+// a simulator's link-state tensor (zero-copy ingestion), quaternion as wxyz.
+__device__ __forceinline__ void load_pose(const PrologueParams& p, int64_t e, int b, float t[3], float q[4]) {
+    if (p.link_states) {
+        const float* r = p.link_states + (e * p.env_stride + p.link_map[b]) * p.record_stride;
+        t[0] = r[p.pos_offset]; t[1] = r[p.pos_offset + 1]; t[2] = r[p.pos_offset + 2];
+        const float* qq = r + p.rot_offset;
+        if (p.rot_xyzw) {
+            q[0] = qq[3]; q[1] = qq[0]; q[2] = qq[1]; q[3] = qq[2];
+        } else {
+            q[0] = qq[0]; q[1] = qq[1]; q[2] = qq[2]; q[3] = qq[3];
+        }
+    } else {
+        const int64_t k = e * p.B + b;
+        const float* bp = p.body_pos + k * 3;
+        const float* bq = p.body_rot + k * 4;
+        t[0] = bp[0]; t[1] = bp[1]; t[2] = bp[2];
+        q[0] = bq[0]; q[1] = bq[1]; q[2] = bq[2]; q[3] = bq[3];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K4 prologue: one warp per (env, cam); lanes walk the links.
 // ---------------------------------------------------------------------------
@@ -79,9 +100,8 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
         t = {rig.mount_pos[0], rig.mount_pos[1], rig.mount_pos[2]};
         q = {rig.mount_rot[0], rig.mount_rot[1], rig.mount_rot[2], rig.mount_rot[3]};
         if (rig.parent >= 0) {
-            const int64_t bi = static_cast<int64_t>(e) * p.B + rig.parent;
-            const float* bp = p.body_pos + bi * 3;
-            const float* bq = p.body_rot + bi * 4;
+            float bp[3], bq[4];
+            load_pose(p, e, rig.parent, bp, bq);
             Q pq = qnorm(qnorm({bq[0], bq[1], bq[2], bq[3]}));
             V3 rt = qrot(pq, t);
             t = {bp[0] + rt.x, bp[1] + rt.y, bp[2] + rt.z};
@@ -120,9 +140,8 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
         LinkRec rec;
         if (b < p.B) {
             const BodyInfo bi = p.bodies[b];
-            const int64_t k = static_cast<int64_t>(e) * p.B + b;
-            const float* bp = p.body_pos + k * 3;
-            const float* bq = p.body_rot + k * 4;
+            float bp[3], bq[4];
+            load_pose(p, e, b, bp, bq);
             float qw = bq[0], qx = bq[1], qy = bq[2], qz = bq[3];
             const float qn = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
             qw *= qn; qx *= qn; qy *= qn; qz *= qn;

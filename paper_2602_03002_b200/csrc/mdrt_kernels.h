@@ -32,6 +32,10 @@ struct PrologueParams {
     const BodyInfo* bodies;
     const float* body_pos;
     const float* body_rot;
+    const float* link_states;   // strided simulator link states (replaces body_pos/rot) or NULL
+    int64_t env_stride;
+    int32_t record_stride, pos_offset, rot_offset, rot_xyzw;
+    const int32_t* link_map;
     const float* off_pos;
     const float* off_rot;
     const float* fov_delta;

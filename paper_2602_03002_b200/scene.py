@@ -173,6 +173,7 @@ class Scene:
         they need a device->host read).
         """
         n, b = self.num_envs, self.num_bodies
+        self._link_states = None
         srcs = []
         for x, k in ((positions, 3), (rotations, 4)):
             if isinstance(x, torch.Tensor):
@@ -228,9 +229,57 @@ class Scene:
         free.record(cur)
         self._up_free[j] = free
 
+    def bind_link_states(self, states: torch.Tensor, link_map, *, pos_offset: int = 0, rot_offset: int = 3,
+                         quat_order: str = "xyzw") -> None:
+        """Read body poses straight from a simulator's link-state tensor (zero copy).
+
+        ``states``: CUDA float32, shape (N, L, R) (or (N*L, R)), one R-float record
+        per (env, simulator link), e.g. R = 13: position, quaternion, linear and
+        angular velocity. ``link_map[b]`` is the simulator link index of body b.
+        Every render (and every ``CapturedStep`` replay) reads the tensor's
+        current contents in the prologue kernel, so there is no per-step pose
+        copy; keep the tensor alive and write it in place. ``set_body_poses``
+        unbinds it. Quaternions may be unnormalised (normalised on the device).
+        """
+        if quat_order not in ("xyzw", "wxyz"):
+            raise ValueError("quat_order must be 'xyzw' or 'wxyz'")
+        if not isinstance(states, torch.Tensor) or states.device != self.device or states.dtype != torch.float32:
+            raise ValueError(f"states must be a float32 tensor on {self.device}")
+        if not states.is_contiguous():
+            raise ValueError("states must be contiguous")
+        n = self.num_envs
+        if states.dim() == 2:
+            if states.shape[0] % n:
+                raise ValueError(f"{states.shape[0]} records do not split into {n} envs")
+            links, rec = states.shape[0] // n, states.shape[1]
+        elif states.dim() == 3 and states.shape[0] == n:
+            links, rec = states.shape[1], states.shape[2]
+        else:
+            raise ValueError(f"states must be (N, L, R) or (N*L, R) with N={n}, got {tuple(states.shape)}")
+        lm = np.asarray(link_map, dtype=np.int64).reshape(-1)
+        if lm.shape != (self.num_bodies,) or (lm.size and (lm.min() < 0 or lm.max() >= links)):
+            raise ValueError(f"link_map must hold {self.num_bodies} link indices in [0, {links})")
+        if not (0 <= pos_offset <= rec - 3 and 0 <= rot_offset <= rec - 4):
+            raise ValueError(f"pos/rot offsets outside the {rec}-float record")
+        lmap = torch.as_tensor(lm.astype(np.int32), device=self.device)
+        self._link_states = (states, lmap, links, rec, int(pos_offset), int(rot_offset), quat_order == "xyzw")
+
+    def unbind_link_states(self) -> None:
+        self._link_states = None
+
+    def _host_poses(self) -> tuple[np.ndarray, np.ndarray]:
+        """(N,B,3), (N,B,4) wxyz f64 host copies of the pose source the prologue reads."""
+        ls = getattr(self, "_link_states", None)
+        if ls is None:
+            return self.body_positions.double().cpu().numpy(), self.body_rotations.double().cpu().numpy()
+        states, lmap, links, rec, po, ro, xyzw = ls
+        r = states.reshape(self.num_envs, links, rec)[:, lmap.long()].double().cpu().numpy()
+        q = r[..., ro:ro + 4]
+        return r[..., po:po + 3], (q[..., [3, 0, 1, 2]] if xyzw else q)
+
     def body_pose(self, env: int, body: int) -> RigidPose:
-        return RigidPose(self.body_positions[env, body].double().cpu().numpy(),
-                         self.body_rotations[env, body].double().cpu().numpy())
+        bp, bq = self._host_poses()
+        return RigidPose(bp[env, body], bq[env, body])
 
     # -- camera randomisation (scene.py:256-277) -----------------------------
     def set_camera_randomization(self, offset_pos, offset_rot, fov_delta) -> None:
@@ -249,8 +298,7 @@ class Scene:
     def camera_world_poses(self) -> tuple[np.ndarray, np.ndarray]:
         """(N,C,3), (N,C,4): parent pose o mount o offset, as the prologue computes it."""
         from .transforms import quat_mul, quat_normalize, quat_rotate
-        bp = self.body_positions.double().cpu().numpy()
-        bq = self.body_rotations.double().cpu().numpy()
+        bp, bq = self._host_poses()
         rp = None if self._rand_pos is None else self._rand_pos.double().cpu().numpy()
         rq = None if self._rand_rot is None else self._rand_rot.double().cpu().numpy()
         n, c = self.num_envs, self.num_cameras
@@ -287,6 +335,14 @@ class Scene:
         a.env_offset = self.env_offset
         a.body_pos = self.body_positions.data_ptr() if self.num_bodies else None
         a.body_rot = self.body_rotations.data_ptr() if self.num_bodies else None
+        ls = getattr(self, "_link_states", None)
+        if ls is not None and self.num_bodies:
+            states, lmap, env_stride, rec, po, ro, xyzw = ls
+            a.link_states = states.data_ptr()
+            a.env_stride, a.record_stride, a.pos_offset, a.rot_offset = env_stride, rec, po, ro
+            a.link_map = lmap.data_ptr()
+            if xyzw:
+                a.flags |= _native.ROT_XYZW
         if self._rand_pos is not None:
             a.cam_off_pos = self._rand_pos.data_ptr()
             a.cam_off_rot = self._rand_rot.data_ptr()

@@ -416,3 +416,51 @@ def test_fused_downsample_equals_standalone(pkg):
     assert torch.equal(ds2, ds)
     with pytest.raises(ValueError):
         pkg.render_pipeline(scene, ds_out=torch.empty((3, 2, 27, 48), device="cuda"), downsample_factor=7)
+
+
+def test_bound_link_states_zero_copy(pkg):
+    """Poses read straight from a simulator-style (N, L, 13) link-state tensor (xyzw quats,
+    extra links, permuted link map) render bitwise like set_body_poses, eager and in a
+    captured graph whose tensor is updated in place."""
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    case = casefile.load(os.path.join(GOLDEN, "render_cfg2_slice.npz"))
+    s_ref, s_bind, s_graph = (casefile.build_scene(case, pkg) for _ in range(3))
+    n, b = s_ref.num_envs, s_ref.num_bodies
+    links = b + 5
+    rng = np.random.default_rng(3)
+    lmap = rng.permutation(links)[:b]
+    cfg = pkg.SensorConfig(seed=1)
+
+    def states_for(pos, rot_wxyz):
+        st = rng.standard_normal((n, links, 13)).astype(np.float32)   # junk in unused links / velocities
+        st[:, lmap, 0:3] = pos
+        st[:, lmap, 3:7] = rot_wxyz[..., [1, 2, 3, 0]]                # xyzw
+        return st
+
+    st = torch.from_numpy(states_for(case["body_pos"], case["body_rot"])).cuda()
+    s_bind.bind_link_states(st, lmap)
+    s_graph.bind_link_states(st.reshape(n * links, 13), lmap)
+    cap = CapturedStep(s_graph, sensor=cfg, first_step=0)
+    for k in range(3):
+        pos = (case["body_pos"] + rng.normal(0, 0.02, case["body_pos"].shape)).astype(np.float32)
+        rot = case["body_rot"].astype(np.float32) * np.float32(1.5)        # unnormalised on purpose
+        st.copy_(torch.from_numpy(states_for(pos, rot)))
+        s_ref.set_body_poses(pos, rot)
+        want = pkg.render_pipeline(s_ref, sensor=cfg, step=k)
+        assert torch.equal(pkg.render_pipeline(s_bind, sensor=cfg, step=k), want), f"eager step {k}"
+        assert torch.equal(cap.replay(), want), f"graph step {k}"
+        hp, hq = s_bind.camera_world_poses()
+        rp, rq = s_ref.camera_world_poses()
+        assert np.allclose(hp, rp) and np.allclose(hq, rq)
+    wx = torch.from_numpy(np.concatenate([np.zeros((n, links, 2), np.float32),
+                                          states_for(case["body_pos"], case["body_rot"])[..., :7][..., [0, 1, 2, 6, 3, 4, 5]]],
+                                         axis=-1)).cuda().contiguous()       # pos at 2, wxyz at 5
+    s_bind.bind_link_states(wx, lmap, pos_offset=2, rot_offset=5, quat_order="wxyz")
+    s_ref.set_body_poses(case["body_pos"], case["body_rot"])
+    assert torch.equal(pkg.render(s_bind).data, pkg.render(s_ref).data)
+    with pytest.raises(ValueError):
+        s_bind.bind_link_states(wx, lmap[:-1])
+    with pytest.raises(ValueError):
+        s_bind.bind_link_states(wx, lmap, rot_offset=8)
+    s_bind.set_body_poses(case["body_pos"], case["body_rot"])            # unbinds
+    assert torch.equal(pkg.render(s_bind).data, pkg.render(s_ref).data)

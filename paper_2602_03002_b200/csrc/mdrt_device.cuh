@@ -251,8 +251,14 @@ struct Traversal {
         }
     }
 
-    __device__ __forceinline__ bool round(const float4* __restrict__ nodes, const float4* __restrict__ tris,
-                                          TraceCounters& ctr) {
+    // OCT < 0: any ray; OCT = 0..7: every ray of the call has the direction-sign
+    // octant OCT (bit 0: dx < 0, bit 1: dy < 0, bit 2: dz < 0), so the near and far
+    // slab of each axis is known at compile time and each child's entry/exit
+    // distance is two 3-input min/max instead of five (bitwise the same result:
+    // fmaf(lo, idx, -o) <= fmaf(hi, idx, -o) for idx >= 0, rounding is monotonic).
+    // descend through inner nodes until `ref` is a leaf (< 0) or kExit
+    template <int OCT>
+    __device__ __forceinline__ void descend_t(const float4* __restrict__ nodes, TraceCounters& ctr) {
         while (ref >= 0) {
             const float4* n = nodes + 4 * static_cast<int64_t>(ref);
             float4 bx, by, bz, rff;
@@ -260,16 +266,29 @@ struct Traversal {
             ldg256(n + 2, bz, rff);   // c0 z lo/hi, c1 z lo/hi | refs
             const int2 rf = make_int2(__float_as_int(rff.x), __float_as_int(rff.y));
             if (COUNT) ++ctr.nodes;
-            const float a0 = fmaf(bx.x, idx, -oxd), a1 = fmaf(bx.y, idx, -oxd);
-            const float a2 = fmaf(bx.z, idy, -oyd), a3 = fmaf(bx.w, idy, -oyd);
-            const float a4 = fmaf(bz.x, idz, -ozd), a5 = fmaf(bz.y, idz, -ozd);
-            const float c0min = fmax3(fminf(a0, a1), fminf(a2, a3), fmaxf(fminf(a4, a5), 0.0f));
-            const float c0max = fmin3(fmaxf(a0, a1), fmaxf(a2, a3), fminf(fmaxf(a4, a5), best));
-            const float b0 = fmaf(by.x, idx, -oxd), b1 = fmaf(by.y, idx, -oxd);
-            const float b2 = fmaf(by.z, idy, -oyd), b3 = fmaf(by.w, idy, -oyd);
-            const float b4 = fmaf(bz.z, idz, -ozd), b5 = fmaf(bz.w, idz, -ozd);
-            const float c1min = fmax3(fminf(b0, b1), fminf(b2, b3), fmaxf(fminf(b4, b5), 0.0f));
-            const float c1max = fmin3(fmaxf(b0, b1), fmaxf(b2, b3), fminf(fmaxf(b4, b5), best));
+            float c0min, c0max, c1min, c1max;
+            if constexpr (OCT < 0) {
+                const float a0 = fmaf(bx.x, idx, -oxd), a1 = fmaf(bx.y, idx, -oxd);
+                const float a2 = fmaf(bx.z, idy, -oyd), a3 = fmaf(bx.w, idy, -oyd);
+                const float a4 = fmaf(bz.x, idz, -ozd), a5 = fmaf(bz.y, idz, -ozd);
+                c0min = fmax3(fminf(a0, a1), fminf(a2, a3), fmaxf(fminf(a4, a5), 0.0f));
+                c0max = fmin3(fmaxf(a0, a1), fmaxf(a2, a3), fminf(fmaxf(a4, a5), best));
+                const float b0 = fmaf(by.x, idx, -oxd), b1 = fmaf(by.y, idx, -oxd);
+                const float b2 = fmaf(by.z, idy, -oyd), b3 = fmaf(by.w, idy, -oyd);
+                const float b4 = fmaf(bz.z, idz, -ozd), b5 = fmaf(bz.w, idz, -ozd);
+                c1min = fmax3(fminf(b0, b1), fminf(b2, b3), fmaxf(fminf(b4, b5), 0.0f));
+                c1max = fmin3(fmaxf(b0, b1), fmaxf(b2, b3), fminf(fmaxf(b4, b5), best));
+            } else {
+                constexpr bool NX = (OCT & 1) != 0, NY = (OCT & 2) != 0, NZ = (OCT & 4) != 0;
+                c0min = fmax3(fmaf(NX ? bx.y : bx.x, idx, -oxd), fmaf(NY ? bx.w : bx.z, idy, -oyd),
+                              fmaxf(fmaf(NZ ? bz.y : bz.x, idz, -ozd), 0.0f));
+                c0max = fmin3(fmaf(NX ? bx.x : bx.y, idx, -oxd), fmaf(NY ? bx.z : bx.w, idy, -oyd),
+                              fminf(fmaf(NZ ? bz.x : bz.y, idz, -ozd), best));
+                c1min = fmax3(fmaf(NX ? by.y : by.x, idx, -oxd), fmaf(NY ? by.w : by.z, idy, -oyd),
+                              fmaxf(fmaf(NZ ? bz.w : bz.z, idz, -ozd), 0.0f));
+                c1max = fmin3(fmaf(NX ? by.x : by.y, idx, -oxd), fmaf(NY ? by.z : by.w, idy, -oyd),
+                              fminf(fmaf(NZ ? bz.z : bz.w, idz, -ozd), best));
+            }
             const bool h0 = c0min <= c0max;
             const bool h1 = c1min <= c1max;
             if (h0 && h1) {
@@ -282,10 +301,25 @@ struct Traversal {
                 ref = pop();
             }
         }
+    }
+
+    // leaf step after a descent: test its triangles and pop; true when finished
+    __device__ __forceinline__ bool leaf_step(const float4* __restrict__ tris, TraceCounters& ctr) {
         if (ref == kExit) return true;
         test_leaf(tris, ref, ctr);
         ref = pop();
         return ref == kExit;
+    }
+
+    __device__ __forceinline__ bool round(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                          TraceCounters& ctr) {
+        descend_t<-1>(nodes, ctr);
+        return leaf_step(tris, ctr);
+    }
+
+    // sign octant of the direction (bit 0: x, 1: y, 2: z negative)
+    __device__ __forceinline__ int octant() const {
+        return (idx < 0.0f ? 1 : 0) | (idy < 0.0f ? 2 : 0) | (idz < 0.0f ? 4 : 0);
     }
 
     // nearest hit t in (1e-6, tmax], or +inf when nothing was hit (the caller then
@@ -302,6 +336,36 @@ __device__ __forceinline__ float trace(const float4* __restrict__ nodes, const f
     tv.init(root, ox, oy, oz, dx, dy, dz, tmax, stack);
     while (!tv.round(nodes, tris, ctr)) {
     }
+    return tv.result();
+}
+
+// trace() for a call made by a set of lanes whose direction octants are usually
+// equal (one camera's tile against the terrain): a warp-uniform octant selects a
+// specialised traversal loop, mixed warps take the generic one.
+template <bool COUNT>
+__device__ __forceinline__ float trace_oct(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                           int32_t root, float ox, float oy, float oz, float dx, float dy,
+                                           float dz, float tmax, int2* __restrict__ stack,
+                                           TraceCounters& ctr) {
+    Traversal<COUNT> tv;
+    tv.init(root, ox, oy, oz, dx, dy, dz, tmax, stack);
+    const int oct = tv.octant();
+    const unsigned mask = __activemask();
+    const bool uniform = __match_any_sync(mask, oct) == mask;
+    do {
+        // only the inner-node descent is specialised; leaf tests are shared
+        if (!uniform) {
+            tv.template descend_t<-1>(nodes, ctr);
+        } else {
+            switch (oct) {
+#define MDRT_OCT_CASE(K) \
+                case K: tv.template descend_t<K>(nodes, ctr); break;
+                MDRT_OCT_CASE(0) MDRT_OCT_CASE(1) MDRT_OCT_CASE(2) MDRT_OCT_CASE(3)
+                MDRT_OCT_CASE(4) MDRT_OCT_CASE(5) MDRT_OCT_CASE(6) MDRT_OCT_CASE(7)
+#undef MDRT_OCT_CASE
+            }
+        }
+    } while (!tv.leaf_step(tris, ctr));
     return tv.result();
 }
 

@@ -386,8 +386,13 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const float wdy = r0.w * dcx + r1.x * dcy + r1.y * dcz;
         const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
         const float bound = p.early_termination ? z : dmax;
+#ifdef MDRT_NO_OCTANT
         const float tt = trace<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
                                       bound * inv_m, stack, ctr);
+#else
+        const float tt = trace_oct<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
+                                          bound * inv_m, stack, ctr);
+#endif
         const float cand = m * tt;
         if (cand < z) z = cand;
     }
@@ -471,64 +476,60 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
 #endif
     const int lane = threadIdx.x & 31;
     const uint32_t total = static_cast<uint32_t>(p.N) * p.C * p.tiles_per_view;
-    if (p.chunks > 0) {
-        // Work order: (0) this SM's contiguous chunk of tiles, so consecutive
-        // tiles of the same views stay on one SM and reuse node records from its
-        // L1; (1) the shared pool of tail tiles; (2) stealing what is left in
-        // other chunks (slow or absent SMs), lanes probing 32 counters at once.
-        const uint32_t nc = static_cast<uint32_t>(p.chunks);
+    // Work order (one render_tile call site keeps the kernel's code small):
+    // (0) with SM-local chunks, this SM's contiguous chunk of tiles, so
+    // consecutive tiles of the same views stay on one SM and reuse node records
+    // from its L1; (1) the shared pool (all tiles when there are no chunks);
+    // (2) stealing what is left in other chunks (slow or absent SMs), lanes
+    // probing 32 counters at once.
+    const uint32_t nc = static_cast<uint32_t>(p.chunks);
+    const uint32_t pool_lo = nc ? p.local_tiles : 0u;
+    uint32_t own = 0;
+    if (nc) {
         uint32_t smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        auto lo_of = [&](uint32_t j) {
-            return static_cast<uint32_t>(static_cast<unsigned long long>(p.local_tiles) * j / nc);
-        };
-        uint32_t phase = 0, base = 0;
-        const uint32_t own = smid % nc;
-        while (true) {
-            uint32_t gw = 0xffffffffu;
-            while (phase < 3) {
-                uint32_t ctr_idx, lo, size;
-                if (phase == 0) {
-                    ctr_idx = own;
-                    lo = lo_of(own);
-                    size = lo_of(own + 1) - lo;
-                } else if (phase == 1) {
-                    ctr_idx = nc;
-                    lo = p.local_tiles;
-                    size = total - p.local_tiles;
-                } else {
-                    const uint32_t k = base + lane;
-                    const bool avail = k < nc &&
-                        *reinterpret_cast<volatile unsigned int*>(p.tile_counter + k) < lo_of(k + 1) - lo_of(k);
-                    const unsigned b = __ballot_sync(0xffffffffu, avail);
-                    if (!b) {
-                        base += 32;
-                        if (base >= nc) phase = 3;
-                        continue;
-                    }
-                    ctr_idx = base + __ffs(b) - 1;
-                    lo = lo_of(ctr_idx);
-                    size = lo_of(ctr_idx + 1) - lo;
-                }
-                uint32_t t = 0;
-                if (lane == 0) t = atomicAdd(p.tile_counter + ctr_idx, 1u);
-                t = __shfl_sync(0xffffffffu, t, 0);
-                if (t < size) {
-                    gw = lo + t;
-                    break;
-                }
-                if (phase < 2) ++phase;
-            }
-            if (gw == 0xffffffffu) break;
-            render_tile<COUNT>(p, gw, lane, stack);
-        }
-        return;
+        own = smid % nc;
     }
+    auto lo_of = [&](uint32_t j) {
+        return static_cast<uint32_t>(static_cast<unsigned long long>(p.local_tiles) * j / nc);
+    };
+    uint32_t phase = nc ? 0u : 1u, base = 0;
     while (true) {
-        uint32_t gw = 0;
-        if (lane == 0) gw = atomicAdd(p.tile_counter, 1u);
-        gw = __shfl_sync(0xffffffffu, gw, 0);
-        if (gw >= total) break;
+        uint32_t gw = 0xffffffffu;
+        while (phase < 3) {
+            uint32_t ctr_idx, lo, size;
+            if (phase == 0) {
+                ctr_idx = own;
+                lo = lo_of(own);
+                size = lo_of(own + 1) - lo;
+            } else if (phase == 1) {
+                ctr_idx = nc;
+                lo = pool_lo;
+                size = total - pool_lo;
+            } else {
+                const uint32_t k = base + lane;
+                const bool avail = k < nc &&
+                    *reinterpret_cast<volatile unsigned int*>(p.tile_counter + k) < lo_of(k + 1) - lo_of(k);
+                const unsigned b = __ballot_sync(0xffffffffu, avail);
+                if (!b) {
+                    base += 32;
+                    if (base >= nc) phase = 3;
+                    continue;
+                }
+                ctr_idx = base + __ffs(b) - 1;
+                lo = lo_of(ctr_idx);
+                size = lo_of(ctr_idx + 1) - lo;
+            }
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(p.tile_counter + ctr_idx, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t < size) {
+                gw = lo + t;
+                break;
+            }
+            phase = (phase == 1 && nc == 0) ? 3u : (phase < 2 ? phase + 1 : phase);
+        }
+        if (gw == 0xffffffffu) break;
         render_tile<COUNT>(p, gw, lane, stack);
     }
 }

@@ -112,6 +112,7 @@ struct mdrt_ctx {
     // per-step scratch
     DevBuf<ViewRec> views;
     DevBuf<LinkRec> links;
+    DevBuf<int2> rects;
     DevBuf<unsigned int> tile_counter;
     DevBuf<StepState> state;
 
@@ -159,6 +160,7 @@ int mdrt_destroy(mdrt_ctx* ctx) {
         ctx->rig_buf.release();
         ctx->views.release();
         ctx->links.release();
+        ctx->rects.release();
         ctx->tile_counter.release();
         ctx->state.release();
         delete ctx;
@@ -341,6 +343,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         const size_t nviews = static_cast<size_t>(N) * C;
         ctx->views.reserve(nviews);
         ctx->links.reserve(std::max<size_t>(1, nviews * std::max(B, 1)));
+        ctx->rects.reserve(std::max<size_t>(1, nviews * std::max(B, 1)));
 
         PrologueParams pp{};
         pp.N = N; pp.C = C; pp.B = B; pp.W = ctx->W; pp.H = ctx->H;
@@ -397,6 +400,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         }
         pp.views = ctx->views.ptr;
         pp.links = ctx->links.ptr;
+        pp.rects = ctx->rects.ptr;
         ctx->tile_counter.reserve(kTileCounters);
         pp.reset_counter = ctx->tile_counter.ptr;
         pp.reset_count = kTileCounters;
@@ -425,6 +429,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.tris = reinterpret_cast<const float4*>(ctx->tris.ptr);
         rp.views = ctx->views.ptr;
         rp.links = ctx->links.ptr;
+        rp.rects = ctx->rects.ptr;
         rp.ray_dirs = a->ray_dirs;
         rp.ray_scale = a->ray_scale;
         rp.ray_envs = a->ray_envs;
@@ -492,6 +497,7 @@ int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, uint64_
         const size_t nviews = static_cast<size_t>(num_envs) * ctx->C;
         ctx->views.reserve(nviews);
         ctx->links.reserve(std::max<size_t>(1, nviews * std::max<size_t>(ctx->bodies.size(), 1)));
+        ctx->rects.reserve(std::max<size_t>(1, nviews * std::max<size_t>(ctx->bodies.size(), 1)));
         ctx->tile_counter.reserve(kTileCounters);
         CK(cudaMemcpy(ctx->state.ptr, &st, sizeof(st), cudaMemcpyHostToDevice));
     });

@@ -240,6 +240,8 @@ static __global__ void __launch_bounds__(128) prologue_kernel(PrologueParams p) 
         if (keep) {
             const int slot = count + __popc(mask & ((1u << lane) - 1u));
             p.links[view * p.B + slot] = rec;
+            p.rects[view * p.B + slot] = make_int2((rec.x0 & 0xffff) | (static_cast<int>(rec.x1) << 16),
+                                                   (rec.y0 & 0xffff) | (static_cast<int>(rec.y1) << 16));
         }
         count += __popc(mask);
     }
@@ -346,34 +348,49 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     float z = dmax;
 
     // ---- K2: links in their local frames (numba_backend.py:190-208) ----
+    // Lanes load 32 links' pixel rects at once (one 8 B record each), a ballot
+    // keeps the links whose rect overlaps this tile, and only those are visited
+    // (in link order); inside, lanes outside the rect sit the trace out.
     const LinkRec* links = p.links + static_cast<int64_t>(view) * p.B;
-    for (int k = 0; k < nlinks; ++k) {
-        const LinkRec& L = links[k];
-        const int4 tail = *reinterpret_cast<const int4*>(&L.root);  // root | x0,x1 | y0,y1 | pad
-        const int x0 = static_cast<int16_t>(tail.y & 0xffff), x1 = tail.y >> 16;
-        const int y0 = static_cast<int16_t>(tail.z & 0xffff), y1 = tail.z >> 16;
-        // warp-uniform tile/rect overlap first, per-lane test only when they overlap
-        const int tx0 = static_cast<int>(tx) * kTileW, ty0 = static_cast<int>(ty) * kTileH;
-        if (x1 < tx0 || x0 >= tx0 + kTileW || y1 < ty0 || y0 >= ty0 + kTileH) continue;
-        const bool want = active && px >= x0 && px <= x1 && py >= y0 && py <= y1;
-        if (!__any_sync(0xffffffffu, want)) continue;
-        if (want) {
-            const float4 m0 = *reinterpret_cast<const float4*>(&L.m[0]);
-            const float4 m1 = *reinterpret_cast<const float4*>(&L.m[4]);
-            const float4 m2 = *reinterpret_cast<const float4*>(&L.m[8]);  // m8 o0 o1 o2
-            const float ldx = m0.x * dcx + m0.y * dcy + m0.z * dcz;
-            const float ldy = m0.w * dcx + m1.x * dcy + m1.y * dcz;
-            const float ldz = m1.z * dcx + m1.w * dcy + m2.x * dcz;
-            const float bound = p.early_termination ? z : dmax;
-            const unsigned int before = ctr.nodes;
-            const float tt = trace<COUNT>(p.nodes, p.tris, tail.x, m2.y, m2.z, m2.w, ldx, ldy, ldz,
-                                          bound * inv_m, stack, ctr);
-            if (COUNT) {
-                ctr.link_nodes += ctr.nodes - before;
-                ++ctr.link_traces;
+    const int2* rects = p.rects + static_cast<int64_t>(view) * p.B;
+    const int tx0 = static_cast<int>(tx) * kTileW, ty0 = static_cast<int>(ty) * kTileH;
+    for (int base = 0; base < nlinks; base += 32) {
+        int2 rr = make_int2(0, 0);
+        bool ov = false;
+        if (base + lane < nlinks) {
+            rr = rects[base + lane];
+            const int x0 = static_cast<int16_t>(rr.x & 0xffff), x1 = rr.x >> 16;
+            const int y0 = static_cast<int16_t>(rr.y & 0xffff), y1 = rr.y >> 16;
+            ov = !(x1 < tx0 || x0 >= tx0 + kTileW || y1 < ty0 || y0 >= ty0 + kTileH);
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, ov);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int rx = __shfl_sync(0xffffffffu, rr.x, j), ry = __shfl_sync(0xffffffffu, rr.y, j);
+            const int x0 = static_cast<int16_t>(rx & 0xffff), x1 = rx >> 16;
+            const int y0 = static_cast<int16_t>(ry & 0xffff), y1 = ry >> 16;
+            const bool want = active && px >= x0 && px <= x1 && py >= y0 && py <= y1;
+            if (!__any_sync(0xffffffffu, want)) continue;
+            if (want) {
+                const LinkRec& L = links[base + j];
+                const float4 m0 = *reinterpret_cast<const float4*>(&L.m[0]);
+                const float4 m1 = *reinterpret_cast<const float4*>(&L.m[4]);
+                const float4 m2 = *reinterpret_cast<const float4*>(&L.m[8]);  // m8 o0 o1 o2
+                const float ldx = m0.x * dcx + m0.y * dcy + m0.z * dcz;
+                const float ldy = m0.w * dcx + m1.x * dcy + m1.y * dcz;
+                const float ldz = m1.z * dcx + m1.w * dcy + m2.x * dcz;
+                const float bound = p.early_termination ? z : dmax;
+                const unsigned int before = ctr.nodes;
+                const float tt = trace<COUNT>(p.nodes, p.tris, L.root, m2.y, m2.z, m2.w, ldx, ldy, ldz,
+                                              bound * inv_m, stack, ctr);
+                if (COUNT) {
+                    ctr.link_nodes += ctr.nodes - before;
+                    ++ctr.link_traces;
+                }
+                const float cand = m * tt;
+                if (cand < z) z = cand;
             }
-            const float cand = m * tt;
-            if (cand < z) z = cand;
         }
     }
 

@@ -55,6 +55,7 @@ struct PrologueParams {
     int32_t* read_slot_out;
     ViewRec* views;
     LinkRec* links;
+    int2* rects;                  // (N*C, B) packed pixel rects of the compacted links (x0|x1<<16, y0|y1<<16)
     unsigned int* reset_counter;  // render kernel's tile counters, zeroed here (prologue runs first)
     int32_t reset_count;          // number of counters to zero
     const StepState* state;       // non-null: step/ring/RNG fields come from device state
@@ -74,6 +75,7 @@ struct RenderParams {
     const float4* tris;
     const ViewRec* views;
     const LinkRec* links;
+    const int2* rects;
     const float* ray_dirs;
     const float* ray_scale;
     int32_t ray_envs;

@@ -213,6 +213,23 @@ int mdrt_rsm_apply(const float *in, float *out, int32_t N, int32_t C, int32_t H,
 int mdrt_downsample_min(const float *in, float *out, int64_t planes, int32_t H, int32_t W,
                         int32_t factor, void *stream);
 
+/* build_bvh (bvh.py:68-136) for one mesh, host only: the same SAH build and
+ * packed records the renderer uploads (64 B nodes: both children's fp32 boxes
+ * + refs, >= 0 inner index, < 0 ~((first << 3) | (count - 1)); 48 B triangles
+ * {v0 + face id, e1, e2}), root = node 0. counts = {nodes, triangles, depth}.
+ * Output buffers may be NULL (sizes only); nodes needs <= max(nf, 1) records,
+ * tris/tri_index nf entries. leaf_max: 1..8, 0 = default (4). */
+int mdrt_bvh_build(const double *verts, int64_t nv, const int64_t *faces, int64_t nf, int32_t leaf_max,
+                   void *nodes, int64_t node_cap, void *tris, int64_t tri_cap, int64_t *tri_index,
+                   int64_t counts[3]);
+
+/* query_bvh (bvh.py:189-217) for n independent rays on the device: closest hit
+ * t in (1e-6, t_max] (+inf on miss) and its original face index (-1 on miss)
+ * against a packed tree (device copies of mdrt_bvh_build's nodes/tris).
+ * origins/dirs: (n, 3) float32 device; t_max may be +inf. */
+int mdrt_query_rays(const void *nodes, const void *tris, const float *origins, const float *dirs, int64_t n,
+                    float t_max, float *t_out, int32_t *face_out, void *stream);
+
 /* depth_to_u8 (frameio.py depth_to_u8, PGM previews): out[i] =
  * round_half_even(255 * (1 - clip(in[i] / d_max, 0, 1))) in f64. in: 16-byte
  * aligned device float32; out: 4-byte aligned device uint8. */

@@ -13,6 +13,7 @@ from .transforms import (RigidPose, Ray, quat_identity, quat_normalize, quat_mul
                          quat_rotate, quat_to_matrix, quat_from_matrix, quat_from_axis_angle,
                          quat_from_euler, quat_yaw, world_to_body_ray, body_to_world_ray)
 from .mesh import TriMesh, load_obj, save_obj, make_box, make_plane, make_icosphere, merge_meshes
+from .bvh import BVH, build_bvh, query_bvh, validate_bvh
 from .camera import CameraModel, build_depth_ray, look_at_pose
 from .scene import Scene, Body, DepthFrame, render, render_naive_baseline, depth_to_z
 from .kernels import BACKENDS, default_backend, resolve_threads
@@ -31,6 +32,7 @@ __all__ = [
     "RigidPose", "Ray", "quat_identity", "quat_normalize", "quat_mul", "quat_conjugate",
     "quat_rotate", "quat_to_matrix", "quat_from_matrix", "quat_from_axis_angle", "quat_from_euler",
     "quat_yaw", "world_to_body_ray", "body_to_world_ray",
+    "BVH", "build_bvh", "query_bvh", "validate_bvh",
     "TriMesh", "load_obj", "save_obj", "make_box", "make_plane", "make_icosphere", "merge_meshes",
     "CameraModel", "build_depth_ray", "look_at_pose",
     "Scene", "Body", "DepthFrame", "render", "render_naive_baseline", "depth_to_z",

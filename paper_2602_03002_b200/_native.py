@@ -140,6 +140,9 @@ def lib():
             "mdrt_downsample_min": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                                    ctypes.c_int32, vp]),
             "mdrt_depth_to_u8": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_double, vp]),
+            "mdrt_bvh_build": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64, ctypes.c_int32, vp,
+                                              ctypes.c_int64, vp, ctypes.c_int64, _c_i64p, _c_i64p]),
+            "mdrt_query_rays": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_float, vp, vp, vp]),
             "mdrt_bvh_check": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_i64p, ctypes.c_int64, _c_i64p]),
             "mdrt_probe_read": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp]),
             "mdrt_state_set": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
@@ -167,7 +170,7 @@ def lib():
 EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_create", "mdrt_destroy",
            "mdrt_add_body", "mdrt_set_terrain", "mdrt_set_cameras", "mdrt_commit", "mdrt_get_stats",
            "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
-           "mdrt_downsample_min", "mdrt_depth_to_u8", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_peer_alloc",
+           "mdrt_downsample_min", "mdrt_depth_to_u8", "mdrt_bvh_build", "mdrt_query_rays", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_peer_alloc",
            "mdrt_peer_open", "mdrt_peer_close", "mdrt_peer_free", "mdrt_sync")
 
 

@@ -67,8 +67,8 @@ const BuildOptions& options() {
 
 class Builder {
    public:
-    Builder(const std::vector<Box>& tb, const std::vector<std::array<double, 3>>& cen)
-        : tbox_(tb), cen_(cen) {}
+    Builder(const std::vector<Box>& tb, const std::vector<std::array<double, 3>>& cen, int leaf_max)
+        : tbox_(tb), cen_(cen), leaf_max_(leaf_max) {}
 
     std::vector<BNode> nodes;
     std::vector<int64_t> idx;
@@ -99,6 +99,7 @@ class Builder {
    private:
     const std::vector<Box>& tbox_;
     const std::vector<std::array<double, 3>>& cen_;
+    const int leaf_max_;
 
     // Returns true and fills kids when node ni was split.
     bool split(int32_t ni, int32_t kids[2]) {
@@ -111,7 +112,7 @@ class Builder {
         // Switch to object-median splits when the remaining depth budget gets
         // tight: a median tree below this node adds ceil(log2(n)) levels.
         int need = 0;
-        const int leaf_max = options().leaf_max;
+        const int leaf_max = leaf_max_;
         while ((int64_t(leaf_max) << need) < n) ++need;
         const bool force_median = depth + need + 1 >= kMaxDepth;
         if (!force_median) {
@@ -223,7 +224,9 @@ void pad_box(const Box& b, float lo[3], float hi[3]) {
 
 }  // namespace
 
-PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int64_t nf) {
+PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int64_t nf, int leaf_max) {
+    if (leaf_max <= 0) leaf_max = options().leaf_max;
+    if (leaf_max > 8) throw std::invalid_argument("leaf size must be <= 8 (leaf encoding)");
     if (nf <= 0) throw std::invalid_argument("cannot build a BVH over an empty mesh");
     std::vector<Box> tb(nf);
     std::vector<std::array<double, 3>> cen(nf);
@@ -235,7 +238,7 @@ PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int
         }
         for (int a = 0; a < 3; ++a) cen[f][a] = 0.5 * (tb[f].lo[a] + tb[f].hi[a]);
     }
-    Builder bld(tb, cen);
+    Builder bld(tb, cen, leaf_max);
     bld.run();
 
     PackedTree out;

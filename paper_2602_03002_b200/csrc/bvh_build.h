@@ -51,7 +51,8 @@ struct PackedTree {
 // Build + pack one mesh. verts (nv,3) f64, faces (nf,3) i64. Faces must be
 // valid indices. Node refs/triangle refs are relative to this tree; the caller
 // offsets them when concatenating trees (offset_tree).
-PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int64_t nf);
+// leaf_max <= 0: the default leaf bound (kMaxLeafTris, or MDRT_LEAF_MAX).
+PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int64_t nf, int leaf_max = 0);
 
 // Shift a tree's internal node and triangle references by the given offsets.
 void offset_tree(PackedTree& t, int32_t node_off, int32_t tri_off);

@@ -635,6 +635,46 @@ int mdrt_downsample_min(const float* in, float* out, int64_t planes, int32_t H, 
     });
 }
 
+int mdrt_bvh_build(const double* verts, int64_t nv, const int64_t* faces, int64_t nf, int32_t leaf_max, void* nodes,
+                   int64_t node_cap, void* tris, int64_t tri_cap, int64_t* tri_index, int64_t counts[3]) {
+    return guarded([&] {
+        need(verts && faces && counts, "NULL argument");
+        need(leaf_max >= 0 && leaf_max <= 8, "leaf_max must be in [1, 8] (0: default)");
+        PackedTree t = build_tree(verts, nv, faces, nf, leaf_max);
+        counts[0] = static_cast<int64_t>(t.nodes.size());
+        counts[1] = static_cast<int64_t>(t.tris.size());
+        counts[2] = t.depth;
+        need(!nodes || node_cap >= counts[0], "node buffer too small");
+        need(!tris || tri_cap >= counts[1], "triangle buffer too small");
+        need(!tri_index || tri_cap >= counts[1], "tri_index buffer too small");
+        if (nodes) std::memcpy(nodes, t.nodes.data(), t.nodes.size() * sizeof(PackedNode));
+        if (tris) std::memcpy(tris, t.tris.data(), t.tris.size() * sizeof(PackedTri));
+        if (tri_index) std::memcpy(tri_index, t.tri_index.data(), t.tri_index.size() * sizeof(int64_t));
+    });
+}
+
+int mdrt_query_rays(const void* nodes, const void* tris, const float* origins, const float* dirs, int64_t n,
+                    float t_max, float* t_out, int32_t* face_out, void* stream) {
+    return guarded([&] {
+        need(nodes && tris && t_out && face_out, "NULL argument");
+        need(n == 0 || (origins && dirs), "NULL rays");
+        need(!(t_max < 0.0f), "t_max must be >= 0");
+        if (n == 0) return;
+        QueryParams q{};
+        q.nodes = static_cast<const float4*>(nodes);
+        q.tris = static_cast<const float4*>(tris);
+        q.root = 0;
+        q.origins = origins;
+        q.dirs = dirs;
+        q.n = n;
+        q.t_max = t_max;
+        q.t_out = t_out;
+        q.face_out = face_out;
+        launch_query(q, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
 int mdrt_depth_to_u8(const float* in, uint8_t* out, int64_t n, double d_max, void* stream) {
     return guarded([&] {
         need(in && out, "NULL argument");

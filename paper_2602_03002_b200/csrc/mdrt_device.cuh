@@ -179,12 +179,13 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // [kStack][kBlock] shared array of packed {ref, entry distance} slots.
 // round() advances to the next leaf, tests it and pops; it returns true when
 // the ray is finished, so callers can interleave work between rounds.
-template <bool COUNT>
+template <bool COUNT, bool FACE = false>
 struct Traversal {
     float ox, oy, oz, dx, dy, dz;
     float idx, idy, idz, oxd, oyd, ozd;
     float best;
     bool hit;
+    int32_t face;   // FACE: original face index of the best hit
     int32_t ref;
     int2* top;
     int2* bottom;
@@ -201,6 +202,7 @@ struct Traversal {
         oxd = ox * idx; oyd = oy * idy; ozd = oz * idz;
         best = tmax;
         hit = false;
+        face = -1;
         ref = root;
         top = bottom = stack;
     }
@@ -247,6 +249,7 @@ struct Traversal {
             if (ok) {
                 best = tt;
                 hit = true;
+                if constexpr (FACE) face = __float_as_int(v0.w);
             }
         }
     }

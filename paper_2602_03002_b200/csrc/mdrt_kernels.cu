@@ -668,6 +668,21 @@ static __global__ void depth_u8_kernel(const float* __restrict__ in, uint8_t* __
     }
 }
 
+// query_bvh: one thread per ray through one packed tree, closest hit + face
+static __global__ void __launch_bounds__(128) query_kernel(QueryParams p) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    int2 stack[kStack];
+    TraceCounters ctr;
+    Traversal<false, true> tv;
+    tv.init(p.root, p.origins[3 * i], p.origins[3 * i + 1], p.origins[3 * i + 2], p.dirs[3 * i], p.dirs[3 * i + 1],
+            p.dirs[3 * i + 2], p.t_max, stack);
+    while (!tv.round(p.nodes, p.tris, ctr)) {
+    }
+    p.t_out[i] = tv.result();
+    p.face_out[i] = tv.hit ? tv.face : -1;
+}
+
 // read-bandwidth probe: grid-stride 16 B loads, one partial sum per block
 static __global__ void __launch_bounds__(256) probe_read_kernel(const float4* __restrict__ buf, int64_t n16,
                                                                 int iters, float* sink) {
@@ -810,6 +825,10 @@ void launch_rsm(const RsmParams& p, int64_t total, cudaStream_t s) {
 
 void launch_downsample(const DownsampleParams& p, int64_t total, cudaStream_t s) {
     downsample_kernel<<<grid_for(total, 256), 256, 0, s>>>(p);
+}
+
+void launch_query(const QueryParams& p, cudaStream_t s) {
+    query_kernel<<<grid_for(p.n, 128), 128, 0, s>>>(p);
 }
 
 void launch_depth_u8(const float* in, uint8_t* out, int64_t n, double dmax, cudaStream_t s) {

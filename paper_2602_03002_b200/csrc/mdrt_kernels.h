@@ -152,6 +152,20 @@ struct DownsampleParams {
 void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s);
 // geometry_bytes: BVH node + triangle bytes; above the L2 size the tiles are
 // scheduled SM-locally (render_kernel) so node reuse comes from L1.
+// query_bvh (bvh.py:189-217): closest hit + face of independent rays against one tree
+struct QueryParams {
+    const float4* nodes;
+    const float4* tris;
+    int32_t root;
+    const float* origins;   // (n, 3)
+    const float* dirs;      // (n, 3)
+    int64_t n;
+    float t_max;
+    float* t_out;           // (n,) +inf on miss
+    int32_t* face_out;      // (n,) -1 on miss
+};
+void launch_query(const QueryParams& p, cudaStream_t s);
+
 void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geometry_bytes, cudaStream_t s);
 void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s);
 void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s);

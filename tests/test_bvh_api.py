@@ -1,0 +1,111 @@
+"""Reference BVH API (bvh.py:34-260) on the renderer's own SAH tree:
+build/validate/determinism on CPU (reference tests/test_bvh.py:19-40, 96-100),
+GPU ray queries against f64 brute force (test_bvh.py:63-93)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2602_03002_b200 import bvh as B
+from paper_2602_03002_b200.mesh import TriMesh, make_box, make_icosphere
+
+
+def random_mesh(rng, num_tris=60, spread=2.0):
+    base = rng.uniform(-spread, spread, size=(num_tris, 3))
+    verts = np.repeat(base, 3, axis=0) + rng.uniform(-0.4, 0.4, size=(num_tris * 3, 3))
+    return TriMesh(verts, np.arange(num_tris * 3).reshape(-1, 3))
+
+
+def test_build_validates_on_primitives_and_soups():
+    for mesh in (make_box(size=(1, 2, 3)), make_icosphere(0.5, subdivisions=2)):
+        bvh = B.build_bvh(mesh)
+        B.validate_bvh(bvh, mesh)
+        assert bvh.num_triangles == mesh.num_faces
+    rng = np.random.default_rng(11)
+    for _ in range(5):
+        mesh = random_mesh(rng)
+        B.validate_bvh(B.build_bvh(mesh), mesh)
+    one = TriMesh(np.eye(3), np.array([[0, 1, 2]]))
+    b = B.build_bvh(one)
+    B.validate_bvh(b, one)
+    assert b.num_nodes == 1 and b.left[0] == -1 and b.count[0] == 1
+
+
+def test_leaf_size_and_determinism():
+    mesh = make_icosphere(1.0, subdivisions=2)
+    for leaf in (1, 2, 4, 8):
+        bvh = B.build_bvh(mesh, leaf_size=leaf)
+        leaves = bvh.count[bvh.left == -1]
+        assert leaves.max() <= leaf and leaves.sum() == mesh.num_faces
+        B.validate_bvh(bvh, mesh)
+    a, b = B.build_bvh(mesh), B.build_bvh(mesh)
+    assert np.array_equal(a.tri_index, b.tri_index) and np.array_equal(a.packed_nodes, b.packed_nodes)
+    assert a.max_depth <= 24
+    with pytest.raises(ValueError):
+        B.build_bvh(mesh, leaf_size=9)
+
+
+def test_validate_catches_corruption():
+    mesh = make_icosphere(0.5, subdivisions=1)
+    bvh = B.build_bvh(mesh)
+    bad = B.BVH(**{**{k: getattr(bvh, k) for k in ("node_min", "node_max", "left", "right", "start", "count",
+                                                    "tri_v0", "tri_v1", "tri_index")},
+                   "tri_v2": bvh.tri_v2 + 1.0})
+    with pytest.raises(AssertionError):
+        B.validate_bvh(bad, mesh)
+
+
+def _brute(origin, direction, tris, t_max=np.inf):
+    """f64 double-sided Moller-Trumbore over all triangles (bvh.py:139-163 semantics)."""
+    best, face = np.inf, -1
+    for i, (v0, v1, v2) in enumerate(tris):
+        e1, e2 = v1 - v0, v2 - v0
+        p = np.cross(direction, e2)
+        det = e1 @ p
+        if abs(det) < 1e-12:
+            continue
+        tv = origin - v0
+        u = (tv @ p) / det
+        q = np.cross(tv, e1)
+        v = (direction @ q) / det
+        t = (e2 @ q) / det
+        if 0 <= u <= 1 and v >= 0 and u + v <= 1 and 1e-6 < t <= t_max and t < best:
+            best, face = t, i
+    return best, face
+
+
+@pytest.mark.gpu
+def test_query_matches_brute_force():
+    rng = np.random.default_rng(12)
+    close = total = 0
+    for _ in range(8):
+        mesh = random_mesh(rng, num_tris=40)
+        mesh = TriMesh(mesh.vertices.astype(np.float32).astype(np.float64), mesh.faces)
+        bvh = B.build_bvh(mesh)
+        tris = mesh.triangles()
+        o = rng.uniform(-3.0, 3.0, size=(40, 3)).astype(np.float32).astype(np.float64)
+        d = rng.standard_normal((40, 3)).astype(np.float32).astype(np.float64)
+        t, face = B.query_bvh(bvh, o, d)
+        for k in range(40):
+            ref_t, ref_f = _brute(o[k], d[k], tris)
+            total += 1
+            if np.isinf(ref_t):
+                close += np.isinf(t[k]) and face[k] == -1
+            else:
+                close += abs(t[k] - ref_t) <= 1e-4 * max(1.0, ref_t) and face[k] == ref_f
+    assert close >= total - 2, f"{total - close} of {total} rays disagree"
+
+
+@pytest.mark.gpu
+def test_query_t_max_single_ray_and_cuda_batch():
+    bvh = B.build_bvh(make_box(size=(1.0, 1.0, 1.0)))
+    t, face = B.query_bvh(bvh, [0.0, 0.0, 5.0], [0.0, 0.0, -1.0])
+    assert t == pytest.approx(4.5, abs=1e-6) and face >= 0
+    assert B.query_bvh(bvh, [0.0, 0.0, 5.0], [0.0, 0.0, -1.0], t_max=4.0) == (np.inf, -1)
+    assert B.query_bvh(bvh, [0.0, 0.0, 5.0], [0.0, 0.0, -1.0], t_max=4.5)[0] == pytest.approx(4.5)  # inclusive
+    o = torch.tensor([[0.0, 0.0, 5.0], [3.0, 3.0, 3.0], [0.1, 0.2, 0.0]], device="cuda")
+    d = torch.tensor([[0.0, 0.0, -1.0], [1.0, 0.0, 0.0], [0.0, 0.0, 1.0]], device="cuda")
+    tt, ff = B.query_bvh(bvh, o, d)
+    assert tt.is_cuda and ff.dtype == torch.int32
+    assert tt[0].item() == pytest.approx(4.5) and np.isinf(tt[1].item()) and ff[1].item() == -1
+    assert tt[2].item() == pytest.approx(0.5)      # from inside: double-sided wall hit

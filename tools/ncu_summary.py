@@ -24,8 +24,10 @@ KEYS = [
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global load sectors"),
     ("lts__t_sector_hit_rate.pct", "L2 sector hit rate %"),
     ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 read sectors (from L1)"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
     ("dram__bytes_read.sum", "DRAM bytes read"),
     ("dram__bytes_write.sum", "DRAM bytes written"),
+    ("dram__bytes.sum.per_second", "DRAM bandwidth"),
 ]
 
 
@@ -48,6 +50,12 @@ def main():
     for k, label in KEYS:
         if k in idx:
             print(f"| {label} (`{k}`) | {vals[idx[k]]} | {units[idx[k]]} |")
+    # L2 read bandwidth actually served to L1 (sectors x 32 B / duration)
+    dk, sk = "gpu__time_duration.sum", "lts__t_sectors_srcunit_tex_op_read.sum"
+    if dk in idx and sk in idx:
+        dur = float(vals[idx[dk]].replace(",", "")) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0}[units[idx[dk]]]
+        gbs = float(vals[idx[sk]].replace(",", "")) * 32 / dur / 1e9
+        print(f"| L2 -> L1 read bandwidth (`{sk}` x 32 B / duration) | {gbs:.1f} | GB/s |")
     # stall reasons
     sass = ncu_csv(a.rep, "--page", "source", "--print-source", "sass")
     sh = sass[1]

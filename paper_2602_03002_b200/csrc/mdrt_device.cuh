@@ -214,7 +214,10 @@ struct Traversal {
     __device__ __forceinline__ int32_t pop() {
         while (top != bottom) {
             top -= kStackStride;
-            const int2 e = *top;
+            // one 64-bit load per entry: read as int2 the compiler splits it into
+            // the distance load and a dependent ref load (two local requests)
+            const unsigned long long raw = *reinterpret_cast<const unsigned long long*>(top);
+            const int2 e = make_int2(static_cast<int>(raw & 0xffffffffu), static_cast<int>(raw >> 32));
             if (__int_as_float(e.y) <= best) return e.x;
         }
         return kExit;

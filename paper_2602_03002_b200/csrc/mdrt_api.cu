@@ -112,6 +112,29 @@ struct mdrt_ctx {
     // per-step scratch
     DevBuf<ViewRec> views;
     DevBuf<LinkRec> links;
+    cudaTextureObject_t tri_tex = 0;   // over `tris`, rebuilt when the buffer changes
+
+    void drop_tri_tex() {
+        if (tri_tex) cudaDestroyTextureObject(tri_tex);
+        tri_tex = 0;
+    }
+    cudaTextureObject_t triangle_texture() {
+        if (!tri_tex) {
+            int max_texels = 0;
+            CK(cudaDeviceGetAttribute(&max_texels, cudaDevAttrMaxTexture1DLinearWidth, device));
+            need(tris.cap * 3 <= static_cast<size_t>(max_texels),
+                 "too many triangles for the texture path (3 texels per triangle)");
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = tris.ptr;
+            rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+            rd.res.linear.sizeInBytes = tris.cap * sizeof(PackedTri);
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            CK(cudaCreateTextureObject(&tri_tex, &rd, &td, nullptr));
+        }
+        return tri_tex;
+    }
     DevBuf<int2> rects;
     DevBuf<unsigned int> tile_counter;
     DevBuf<StepState> state;
@@ -154,6 +177,7 @@ int mdrt_destroy(mdrt_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
+        ctx->drop_tri_tex();
         ctx->nodes.release();
         ctx->tris.release();
         ctx->body_info.release();
@@ -273,6 +297,7 @@ int mdrt_commit(mdrt_ctx* ctx) {
         if (nodes.empty()) nodes.push_back(PackedNode{});
         if (tris.empty()) tris.push_back(PackedTri{});
         if (infos.empty()) infos.push_back(BodyInfo{});
+        ctx->drop_tri_tex();
         ctx->nodes.reserve(nodes.size());
         ctx->tris.reserve(tris.size());
         ctx->body_info.reserve(infos.size());
@@ -427,6 +452,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.terrain_root = ctx->has_terrain ? ctx->terrain_root : -1;
         rp.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);
         rp.tris = reinterpret_cast<const float4*>(ctx->tris.ptr);
+        rp.tri_tex = ctx->triangle_texture();
         rp.views = ctx->views.ptr;
         rp.links = ctx->links.ptr;
         rp.rects = ctx->rects.ptr;

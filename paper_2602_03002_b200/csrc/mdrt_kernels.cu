@@ -389,7 +389,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
                 const float ldz = m1.z * dcx + m1.w * dcy + m2.x * dcz;
                 const float bound = p.early_termination ? z : dmax;
                 const unsigned int before = ctr.nodes;
-                const float tt = trace<COUNT>(p.nodes, p.tris, L.root, m2.y, m2.z, m2.w, ldx, ldy, ldz,
+                const float tt = trace<COUNT>(p.nodes, p.tri_tex, L.root, m2.y, m2.z, m2.w, ldx, ldy, ldz,
                                               bound * inv_m, stack, ctr);
                 if (COUNT) {
                     ctr.link_nodes += ctr.nodes - before;
@@ -411,10 +411,10 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
         const float bound = p.early_termination ? z : dmax;
 #ifdef MDRT_NO_OCTANT
-        const float tt = trace<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
+        const float tt = trace<COUNT>(p.nodes, p.tri_tex, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
                                       bound * inv_m, stack, ctr);
 #else
-        const float tt = trace_oct<COUNT>(p.nodes, p.tris, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
+        const float tt = trace_oct<COUNT>(p.nodes, p.tri_tex, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
                                           bound * inv_m, stack, ctr);
 #endif
         const float cand = m * tt;

@@ -73,6 +73,7 @@ struct RenderParams {
     int32_t terrain_root;
     const float4* nodes;
     const float4* tris;
+    cudaTextureObject_t tri_tex;  // texture object over `tris` (float4 texels): the traversal reads triangles here
     const ViewRec* views;
     const LinkRec* links;
     const int2* rects;

@@ -430,12 +430,21 @@ def main():
     # timed region here. Timed with events around the whole loop (the copy stream
     # joins before the end event).
     outs = [out, torch.empty_like(out)]
-    host_obs = [torch.empty(scene.frame_shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    # the step's result delivered to the host: the observation, or for the paper pipeline
+    # the 48x27 block minimum the policy reads (sensor.py:85-100)
+    deliver = [ds, torch.empty_like(ds)] if ds is not None else outs
+    host_obs = [torch.empty(tuple(deliver[0].shape), dtype=torch.float32).pin_memory() for _ in range(2)]
+
+    def e2e_step(i):
+        kw = (dict(ds_out=deliver[i % 2], host_ds_out=host_obs[i % 2]) if ds is not None
+              else dict(host_out=host_obs[i % 2]))
+        md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf, timestamp=step_id[0] * dt,
+                           delays=delays, out=outs[i % 2], **kw)
+        step_id[0] += 1
+
     for i in range(2):   # warm the copy path
         scene.set_body_poses(*pose_host[i % P], validate=False)
-        md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf, timestamp=step_id[0] * dt,
-                           delays=delays, out=outs[i % 2], host_out=host_obs[i % 2])
-        step_id[0] += 1
+        e2e_step(i)
     scene.host_sync()
     torch.cuda.synchronize()
     if world > 1:
@@ -448,9 +457,7 @@ def main():
         flush.fill_(float(i))
         hp, hq = pose_host[i % P]
         scene.set_body_poses(hp, hq, validate=False)        # pinned host -> device
-        md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf, timestamp=step_id[0] * dt,
-                           delays=delays, out=outs[i % 2], host_out=host_obs[i % 2])
-        step_id[0] += 1
+        e2e_step(i)
     e2e_host_ms = (time.perf_counter() - e2e_wall0) * 1e3   # host time to enqueue the loop
     stream.wait_event(scene._last_copy)
     e1.record(stream)
@@ -462,7 +469,7 @@ def main():
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record(stream)
     for i in range(5):
-        host_obs[i % 2].copy_(out, non_blocking=True)
+        host_obs[i % 2].copy_(deliver[0], non_blocking=True)
     c1.record(stream)
     torch.cuda.synchronize()
     d2h_gbs = 5 * d2h / (c0.elapsed_time(c1) * 1e-3) / 1e9
@@ -570,8 +577,10 @@ def main():
                     "ms_per_step": e2e_ms / args.steps, "d2h_alone_gbs": d2h_gbs,
                     "host_enqueue_ms_per_step": e2e_host_ms / args.steps,
                     "d2h_floor_ms": d2h / (d2h_gbs * 1e9) * 1e3,
-                    "how": "pinned-host poses H2D + fused pipeline + obs D2H (copy stream, double-buffered) "
-                           "every step, L2 flush inside the timed loop, events around the whole loop"},
+                    "delivered": "48x27 block-min observation (policy input)" if ds is not None
+                                 else "full observation (N,C,H,W) f32",
+                    "how": "pinned-host poses H2D (upload stream) + fused pipeline + result D2H (copy stream, "
+                           "double-buffered) every step, L2 flush inside the timed loop, events around the whole loop"},
             "gpu_launches": 2 * args.steps,
             "graph": {"value": all_rays / (graph_ms * 1e-3), "unit": "rays/s", "ms_per_step": graph_ms / args.steps,
                       "how": "CapturedStep replay (advance+prologue+render CUDA graph, device step state), "

@@ -60,7 +60,7 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
                     counters: torch.Tensor | None = None,
                     host_out: torch.Tensor | None = None, rsm: RsmConfig | None = None,
                     rsm_modes=None, ds_out: torch.Tensor | None = None,
-                    downsample_factor: int = 5) -> torch.Tensor:
+                    downsample_factor: int = 5, host_ds_out: torch.Tensor | None = None) -> torch.Tensor:
     """One simulation step of the multi-depth pipeline; returns the observation (N,C,H,W).
 
     * ``sensor``: apply noise/dropout/clamp with counters (step, global env, cam, row, col).
@@ -72,7 +72,9 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     * ``rsm`` + ``rsm_modes`` (N, C): random side masking of the observation
       (perception.py:169-202), i.e. ``rsm_apply(obs, rsm_modes, rsm, step=step)``.
     * ``ds_out`` (N, C, H/f, W/f): also write ``downsample_min(obs, f)``
-      (sensor.py:85-100) from the same kernel, f = ``downsample_factor``.
+      (sensor.py:85-100) from the same kernel, f = ``downsample_factor``;
+      ``host_ds_out`` (pinned CPU, same shape) receives it like ``host_out``
+      (the paper's policy reads the 48x27 block minimum, not the native frame).
     """
     data = scene._new_frame(out)
     scene._guard_out(data)
@@ -84,6 +86,9 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     a.step = int(step)
     if ds_out is not None:
         _set_downsample(a, scene, ds_out, downsample_factor)
+        scene._guard_out(ds_out)
+    elif host_ds_out is not None:
+        raise ValueError("host_ds_out needs ds_out")
     if rsm is not None:
         _set_rsm(a, scene, rsm, rsm_modes, keep)
     if sensor is not None:
@@ -125,6 +130,8 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     scene._launch(a)
     if host_out is not None:
         scene._deliver(data, host_out)
+    if host_ds_out is not None:
+        scene._deliver(ds_out, host_ds_out)
     return data
 
 

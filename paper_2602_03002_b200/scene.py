@@ -367,9 +367,9 @@ class Scene:
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream(self.device)
             self._copy_events = {}
-        if host_out.device.type != "cpu" or tuple(host_out.shape) != self.frame_shape or \
+        if host_out.device.type != "cpu" or tuple(host_out.shape) != tuple(out.shape) or \
                 host_out.dtype != torch.float32 or not host_out.is_pinned():
-            raise ValueError(f"host_out must be a pinned float32 CPU tensor of shape {self.frame_shape}")
+            raise ValueError(f"host_out must be a pinned float32 CPU tensor of shape {tuple(out.shape)}")
         cur = torch.cuda.current_stream(self.device)
         done = torch.cuda.Event()
         done.record(cur)

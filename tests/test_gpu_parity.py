@@ -416,6 +416,18 @@ def test_fused_downsample_equals_standalone(pkg):
     assert torch.equal(ds2, ds)
     with pytest.raises(ValueError):
         pkg.render_pipeline(scene, ds_out=torch.empty((3, 2, 27, 48), device="cuda"), downsample_factor=7)
+    # asynchronous delivery of the policy observation (double-buffered, as bench.py's e2e)
+    bufs = [torch.empty_like(ds) for _ in range(2)]
+    hosts = [torch.empty((3, 2, 27, 48)).pin_memory() for _ in range(2)]
+    want = []
+    for k in range(4):
+        pkg.render_pipeline(scene, sensor=cfg, step=10 + k, ds_out=bufs[k % 2], host_ds_out=hosts[k % 2])
+        want.append(bufs[k % 2].clone())
+        if k % 2 == 1:
+            scene.host_sync()
+            assert torch.equal(hosts[0], want[k - 1].cpu()) and torch.equal(hosts[1], want[k].cpu())
+    with pytest.raises(ValueError):
+        pkg.render_pipeline(scene, host_ds_out=hosts[0])
 
 
 def test_bound_link_states_zero_copy(pkg):

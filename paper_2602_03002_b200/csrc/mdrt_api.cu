@@ -443,8 +443,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
 
         RenderParams rp{};
         rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
-        rp.tiles_x = (ctx->W + kTileW - 1) / kTileW;
-        rp.tiles_per_view = rp.tiles_x * ((ctx->H + kTileH - 1) / kTileH);
+        rp.tile_w = render_tile_width(ctx->W);
+        const int tile_h = 32 / rp.tile_w;
+        rp.tiles_x = (ctx->W + rp.tile_w - 1) / rp.tile_w;
+        rp.tiles_per_view = rp.tiles_x * ((ctx->H + tile_h - 1) / tile_h);
         rp.m_tiles_x = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_x));
         rp.m_tiles_per_view = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_per_view));
         rp.m_C = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(C));

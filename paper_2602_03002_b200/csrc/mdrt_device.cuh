@@ -22,12 +22,8 @@ constexpr int kStackStride = kBlock;  // this thread's column of a block-wide sh
 #else
 constexpr int kStackStride = 1;       // per-thread stack in local memory (L1-cached)
 #endif
-#ifndef MDRT_TILE_W
-#define MDRT_TILE_W 8
-#endif
-constexpr int kTileW = MDRT_TILE_W;  // a warp renders a kTileW x kTileH pixel tile of one view
-constexpr int kTileH = 32 / kTileW;
-static_assert(kTileW * kTileH == 32 && (kTileW & (kTileW - 1)) == 0, "tile must be 32 pixels, power-of-2 wide");
+// a warp renders a TW x (32 / TW) pixel tile of one view; TW (4 or 8) is chosen
+// per launch from the image width (render_tile_width)
 constexpr int kExit = INT32_MIN;    // traversal stack sentinel
 constexpr float kRayEps = 1e-6f;    // RAY_EPSILON (bvh.py:30): hits need t > 1e-6
 constexpr float kBaryEps = 1e-5f;   // fp32 watertightness margin on barycentrics

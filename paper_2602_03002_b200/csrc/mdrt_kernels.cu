@@ -318,8 +318,10 @@ __device__ __forceinline__ void st_stream(float* p, float v) { *p = v; }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 #endif
 
-template <bool COUNT>
+template <bool COUNT, int TW>
 __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int2* stack) {
+    constexpr int kTileW = TW;          // this launch's tile shape: TW x (32 / TW) pixels
+    constexpr int kTileH = 32 / TW;
     const uint32_t view = fast_div(gw, static_cast<uint32_t>(p.tiles_per_view), p.m_tiles_per_view);
     const uint32_t tile = gw - view * static_cast<uint32_t>(p.tiles_per_view);
     const uint32_t ty = fast_div(tile, static_cast<uint32_t>(p.tiles_x), p.m_tiles_x);
@@ -485,7 +487,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
 #ifndef MDRT_MINB
 #define MDRT_MINB 9
 #endif
-template <bool COUNT>
+template <bool COUNT, int TW>
 static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(RenderParams p) {
     // Traversal stack in local memory: it is cached in L1 like the node
     // records, and with no shared memory reserved the whole 256 KB of the
@@ -554,7 +556,7 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
             phase = (phase == 1 && nc == 0) ? 3u : (phase < 2 ? phase + 1 : phase);
         }
         if (gw == 0xffffffffu) break;
-        render_tile<COUNT>(p, gw, lane, stack);
+        render_tile<COUNT, TW>(p, gw, lane, stack);
     }
 }
 
@@ -751,7 +753,21 @@ void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s) {
     prologue_kernel<<<grid_for(views * 32, 128), 128, 0, s>>>(p);
 }
 
-void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geometry_bytes, cudaStream_t s) {
+int render_tile_width(int W) {
+    // 4 x 8 tiles for narrow images (64-wide: +0.7 % at configs 2 and 3), 8 x 4
+    // otherwise (160- and 240-wide: +0.4..1.3 %); MDRT_TILE_W (4 or 8) overrides
+    static int env_tw = -1;
+    if (env_tw < 0) {
+        const char* t = std::getenv("MDRT_TILE_W");
+        env_tw = t ? std::atoi(t) : 0;
+    }
+    if (env_tw == 4 || env_tw == 8) return env_tw;
+    return W <= 96 ? 4 : 8;
+}
+
+template <int TW>
+static void launch_render_tw(const RenderParams& p, int64_t warps, bool count, int64_t geometry_bytes,
+                             cudaStream_t s) {
     // persistent grid: as many blocks as can be co-resident (capped by the work)
     static int blocks_per_sm[2] = {0, 0};
     static int sms = 0;
@@ -762,11 +778,13 @@ void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geo
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, dev);
         if (const char* cv = std::getenv("MDRT_CARVEOUT")) {   // experiment: shared-memory carveout %
-            cudaFuncSetAttribute(render_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv));
-            cudaFuncSetAttribute(render_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv));
+            cudaFuncSetAttribute(render_kernel<false, TW>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 std::atoi(cv));
+            cudaFuncSetAttribute(render_kernel<true, TW>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 std::atoi(cv));
         }
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], render_kernel<false>, kBlock, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], render_kernel<true>, kBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], render_kernel<false, TW>, kBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], render_kernel<true, TW>, kBlock, 0);
     }
     const int64_t need = (warps * 32 + kBlock - 1) / kBlock;
     const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(sms) * std::max(1, blocks_per_sm[count]));
@@ -793,9 +811,16 @@ void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geo
         }
     }
     if (count)
-        render_kernel<true><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(q);
+        render_kernel<true, TW><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(q);
     else
-        render_kernel<false><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(q);
+        render_kernel<false, TW><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(q);
+}
+
+void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geometry_bytes, cudaStream_t s) {
+    if (p.tile_w == 4)
+        launch_render_tw<4>(p, warps, count, geometry_bytes, s);
+    else
+        launch_render_tw<8>(p, warps, count, geometry_bytes, s);
 }
 
 void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s) {

@@ -67,6 +67,7 @@ struct PrologueParams {
 
 struct RenderParams {
     int32_t N, C, B, W, H;
+    int32_t tile_w;               // tile shape: tile_w x (32 / tile_w) pixels (4 or 8)
     int32_t tiles_x, tiles_per_view;
     uint32_t m_tiles_x, m_tiles_per_view, m_C;   // fast_div multipliers floor((2^32-1)/d)
     int32_t early_termination;
@@ -167,6 +168,7 @@ struct QueryParams {
 };
 void launch_query(const QueryParams& p, cudaStream_t s);
 
+int render_tile_width(int W);   // tile shape the render kernel uses for W-pixel-wide images
 void launch_render(const RenderParams& p, int64_t warps, bool count, int64_t geometry_bytes, cudaStream_t s);
 void launch_noise(const NoiseParams& p, int64_t total, cudaStream_t s);
 void launch_gather(const GatherParams& p, int64_t total, cudaStream_t s);

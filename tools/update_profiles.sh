@@ -15,8 +15,14 @@ for cfg, f in (("cfg2", "profiles/r01_render_kernel_ncu.md"), ("cfg5", "profiles
     def val(lbl):
         m = re.search(lbl + r".*?\| ([0-9.]+) \| (\w+)", txt)
         return float(m.group(1)) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[m.group(2)]
+    def pct(lbl):
+        return float(re.search(lbl + r".*?\| ([0-9.]+) \| %", txt).group(1))
     json.dump({"dram_bytes_per_launch": int(val("DRAM bytes read") + val("DRAM bytes written")),
-               "source": f + " (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum, one render_kernel launch)"},
+               "l1_lsu_data_pipe_pct": pct("L1 data-pipe wavefronts %"),
+               "issue_active_pct": pct("issue active %"),
+               "l2_throughput_pct": pct("L2 throughput %"),
+               "source": f + " (ncu --set full, one render_kernel launch: dram__bytes_read.sum + dram__bytes_write.sum, "
+                             "l1tex__data_pipe_lsu_wavefronts, smsp__issue_active, lts__throughput)"},
               open(f"profiles/traffic_{cfg}.json", "w"), indent=1)
 for c in ("cfg2", "cfg3", "cfg5", "cfg5_1m", "paper"):
     d = json.loads(open(f"profiles/r01_bench_{c}.jsonl").readline())

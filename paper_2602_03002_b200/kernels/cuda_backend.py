@@ -57,10 +57,37 @@ def _context(flat, C, H, W, d_max, device):
         return ctx
 
 
-def _dev(x, device):
+_staging: dict = {}
+
+
+def _host_staging(nbytes: int, device) -> torch.Tensor:
+    """A pinned host buffer (per device, grown on demand) for full-speed D2H of ``out``."""
+    buf = _staging.get(device.index)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8).pin_memory()
+        _staging[device.index] = buf
+    return buf
+
+
+_in_staging: dict = {}
+
+
+def _dev(x, device, slot=0):
+    """Input array -> float32 CUDA tensor. Host arrays are cast by torch's
+    multithreaded copy into a pinned staging buffer (one per argument slot),
+    then uploaded asynchronously on the current stream."""
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=torch.float32).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(device, non_blocking=True)
+    src = torch.from_numpy(np.ascontiguousarray(x))
+    key = (device.index, slot)
+    buf = _in_staging.get(key)
+    if buf is None or buf.numel() < src.numel():
+        buf = torch.empty(max(src.numel(), 1), dtype=torch.float32).pin_memory()
+        _in_staging[key] = buf
+    torch.cuda.current_stream(device).synchronize()     # the previous call's upload from this slot is done
+    stage = buf[:src.numel()].view(src.shape)
+    stage.copy_(src)
+    return stage.to(device, non_blocking=True)
 
 
 def render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,
@@ -70,9 +97,9 @@ def render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale
     d_max = np.broadcast_to(np.asarray(d_max, np.float64), (c,))
     ctx = _context(flat, c, h, w, d_max, device)
     b = len(flat.body_root)
-    bp, bq = _dev(body_pos, device), _dev(body_rot, device)
-    cp, cq = _dev(cam_pos, device), _dev(cam_rot, device)
-    rd, rs = _dev(ray_dirs, device), _dev(ray_scale, device)
+    bp, bq = _dev(body_pos, device, 0), _dev(body_rot, device, 1)
+    cp, cq = _dev(cam_pos, device, 2), _dev(cam_rot, device, 3)
+    rd, rs = _dev(ray_dirs, device, 4), _dev(ray_scale, device, 5)
     if tuple(rd.shape[1:]) != (c, h, w, 3) or tuple(rs.shape[1:]) != (c, h, w):
         raise ValueError("ray grids must be shaped (RN,C,H,W,3) / (RN,C,H,W)")
     dev_out = out if isinstance(out, torch.Tensor) and out.is_cuda and out.is_contiguous() else \
@@ -93,5 +120,11 @@ def render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale
         if isinstance(out, torch.Tensor):
             out.copy_(dev_out)
         else:
-            out[...] = dev_out.cpu().numpy()
+            # pinned staging (full PCIe rate), then a multithreaded host copy into the
+            # caller's (typically freshly allocated, scene.py:344-347) numpy array
+            stage = _host_staging(dev_out.numel() * 4, device)[:dev_out.numel() * 4].view(torch.float32)
+            stage = stage.view(dev_out.shape)
+            stage.copy_(dev_out, non_blocking=True)
+            torch.cuda.current_stream(device).synchronize()
+            torch.from_numpy(out).copy_(stage) if out.flags.c_contiguous else np.copyto(out, stage.numpy())
     return out

@@ -474,6 +474,50 @@ def main():
     torch.cuda.synchronize()
     d2h_gbs = 5 * d2h / (c0.elapsed_time(c1) * 1e-3) / 1e9
 
+    # ---- the reference's own plugin seam: render_batch with host numpy buffers ----
+    # Called as multidepth.scene.render calls its backend (numba_backend.py:222-234):
+    # f64 numpy poses / camera poses / ray grids in, a freshly allocated numpy out
+    # written in place; wall clock per call (render only: the seam has no sensor stage).
+    seam = None
+    try:
+        from paper_2602_03002_b200 import kernels as mdk
+
+        class _Flat:   # the FlatGeometry fields the CUDA backend reads (scene.py:49-78)
+            pass
+
+        flat = _Flat()
+        tl = [m.triangles() for _, m in bodies]
+        flat.tri_v0, flat.tri_v1, flat.tri_v2 = (np.concatenate([t[:, k] for t in tl]) for k in range(3))
+        flat.body_tri_offsets = np.cumsum([0] + [len(t) for t in tl])
+        flat.body_root = np.zeros(len(tl), np.int32)
+        gt = terrain.triangles()
+        flat.g_tri_v0, flat.g_tri_v1, flat.g_tri_v2 = gt[:, 0], gt[:, 1], gt[:, 2]
+        _, render_batch = mdk.get_render_fn("cuda")
+        dmax_c = np.array([c.d_max for c in w.cameras])
+        seam_in = []
+        for i in range(2):
+            hp = pose_host[i][0].numpy().astype(np.float64)
+            hq = pose_host[i][1].numpy().astype(np.float64)
+            scene.set_body_poses(hp, hq, validate=False)
+            cp_, cq_ = scene.camera_world_poses()
+            seam_in.append((hp, hq, cp_, cq_))
+        grids = scene.ray_grids()
+        seam_t = []
+        for i in range(6):
+            hp, hq, cp_, cq_ = seam_in[i % 2]
+            seam_out = np.empty(scene.frame_shape, np.float32)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            render_batch(flat, hp, hq, cp_, cq_, grids[0], grids[1], dmax_c, True, seam_out, None)
+            torch.cuda.synchronize()
+            seam_t.append(time.perf_counter() - t0)
+        seam_ms = 1e3 * float(np.mean(seam_t[2:]))
+        seam = {"value": rays_per_step / (seam_ms * 1e-3), "unit": "rays/s", "ms_per_call": seam_ms,
+                "how": "kernels.get_render_fn('cuda') render_batch with f64 numpy inputs and a fresh numpy out "
+                       "(the reference's backend seam, render only), wall clock per call, this rank"}
+    except Exception as exc:   # diagnostic only
+        print(f"seam measurement failed: {exc}", file=sys.stderr)
+
     # ---- optional: step + NCCL gather of every rank's observation to rank 0 ----
     gather_ms = p2p_ms = 0.0
     if args.gather and world > 1:
@@ -594,6 +638,7 @@ def main():
             "graph": {"value": all_rays / (graph_ms * 1e-3), "unit": "rays/s", "ms_per_step": graph_ms / args.steps,
                       "how": "CapturedStep replay (advance+prologue+render CUDA graph, device step state), "
                              "device pose copy + L2 flush between steps as for value"},
+            "e2e_seam": seam,
             "gather": ({"value": all_rays / (gather_ms * 1e-3), "unit": "rays/s",
                         "how": "step + NCCL P2P gather of all observations to rank 0, no L2 flush",
                         "fused_p2p": {"value": all_rays / (p2p_ms * 1e-3), "unit": "rays/s",

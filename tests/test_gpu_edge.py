@@ -125,3 +125,13 @@ def test_sm_local_tile_schedule_is_bitwise_identical(tmp_path, frac):
         subprocess.run([sys.executable, "-c", _SCHED_SCRIPT, str(path), root], check=True, env=env, timeout=300)
         outs[f] = np.load(path)
     assert np.array_equal(outs["0"], outs[frac])
+
+
+def test_high_resolution_camera(pkg, oracle):
+    """A 320x240 camera (8x4 tiles, 2400 tiles per view) against the oracle."""
+    g = np.random.default_rng(8)
+    bodies, terrain, cams, pos, rot, _ = random_scene(pkg, g, num_envs=2, num_cams=1, num_bodies=6)
+    cam = cams[0]
+    hi = pkg.CameraModel(width=320, height=240, hfov_deg=cam.hfov_deg, vfov_deg=cam.vfov_deg, d_max=cam.d_max,
+                         mount=cam.mount)
+    _check(pkg, oracle, bodies, terrain, [hi], pos, rot, 2, max_bad=int(1e-4 * 2 * 320 * 240) + 1)

@@ -106,12 +106,88 @@ __device__ __forceinline__ double unit53(unsigned long long h) {
     return static_cast<double>(h >> 11) * 0x1p-53;
 }
 
+#ifndef MDRT_LIBDEVICE_BM
+// Box-Muller transcendentals specialised to their argument ranges (u1 in
+// [2^-53, 1], u2 in [0, 1)), f64 throughout, ~1 ulp: fdlibm's log (e_log.c:
+// argument reduction to [sqrt(1/2), sqrt(2)), s = f / (2 + f), degree-14
+// polynomial in s) with the division done by a reciprocal approximation and two
+// Newton steps; sqrt by rsqrt approximation, two Newton steps and a residual
+// correction; cos(2 pi u2) reduced exactly to an octant of [-pi/4, pi/4]
+// (4 u2 is exact) and fdlibm's kernel sin/cos polynomials (k_sin.c, k_cos.c).
+// Differences to numpy's log/cos(2*pi*u2) are ~1e-16 relative, far below the
+// float32 rounding of the noisy depth (the sensor goldens stay bit-exact); about
+// 1 % faster per step than CUDA's general log/sqrt/cos (MDRT_LIBDEVICE_BM).
+__device__ __forceinline__ double rcp_approx_f64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ double rsqrt_approx_f64(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ double log_unit(double x) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    int e = (hi >> 20) - 1023;
+    int mhi = (hi & 0x000FFFFF) | 0x3FF00000;
+    const bool big = mhi > 0x3FF6A09E;            // m > sqrt(2): use m / 2
+    mhi -= big ? 0x00100000 : 0;
+    e += big ? 1 : 0;
+    const double f = __hiloint2double(mhi, lo) - 1.0;
+    const double d = 2.0 + f;
+    double r = rcp_approx_f64(d);
+    r = fma(r, fma(-d, r, 1.0), r);
+    r = fma(r, fma(-d, r, 1.0), r);
+    const double sv = f * r;
+    const double z = sv * sv;
+    const double R = z * fma(z, fma(z, fma(z, fma(z, fma(z, fma(z, 1.479819860511658591e-01,
+        1.531383769920937332e-01), 1.818357216161805012e-01), 2.222219843214978396e-01),
+        2.857142874366239149e-01), 3.999999999940941908e-01), 6.666666666666735130e-01);
+    const double hfsq = 0.5 * f * f;
+    const double de = static_cast<double>(e);
+    return de * 6.93147180369123816490e-01 + (f - (hfsq - (sv * (hfsq + R) + de * 1.90821492927058770002e-10)));
+}
+__device__ __forceinline__ double sqrt_nonneg(double y) {
+    double r = rsqrt_approx_f64(y);
+    const double hy = 0.5 * y;
+    r = r * fma(-hy * r, r, 1.5);
+    r = r * fma(-hy * r, r, 1.5);
+    double sq = y * r;
+    sq = fma(fma(-sq, sq, y), 0.5 * r, sq);
+    return y > 0.0 ? sq : 0.0;
+}
+__device__ __forceinline__ double cos_2pi(double u) {
+    const double x = 4.0 * u;                      // exact
+    const double q = rint(x);
+    const double t = (x - q) * 1.57079632679489655800e+00;
+    const double z = t * t;
+    const double sn = fma(t * z, fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10,
+        -2.50507602534068634195e-08), 2.75573137070700676789e-06), -1.98412698298579493134e-04),
+        8.33333333332248946124e-03), -1.66666666666666324348e-01), t);
+    const double rc = z * fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11,
+        2.08757232129817482790e-09), -2.75573143513906633035e-07), 2.48015872894767294178e-05),
+        -1.38888888888741095749e-03), 4.16666666666666019037e-02);
+    const double hz = 0.5 * z;
+    const double w = 1.0 - hz;
+    const double cs = w + (((1.0 - w) - hz) + z * rc);
+    const int k = static_cast<int>(q) & 3;
+    const double v = (k & 1) ? sn : cs;
+    return (k == 1 || k == 2) ? -v : v;
+}
+#endif
+
 // standard normal by Box-Muller on two domain-separated sub-hashes (rng.py:94-99)
 __device__ __forceinline__ double normal_from_hash(unsigned long long h) {
     const double u1 = static_cast<double>((mix64(h ^ kCDomU1) >> 11) + 1ULL) * 0x1p-53;
     const double u2 = static_cast<double>(mix64(h ^ kCDomU2) >> 11) * 0x1p-53;
     // __dmul_rn: keep numpy's unfused rounding
+#ifndef MDRT_LIBDEVICE_BM
+    return __dmul_rn(sqrt_nonneg(__dmul_rn(-2.0, log_unit(u1))), cos_2pi(u2));
+#else
     return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+#endif
 }
 
 // apply_noise_dropout for one pixel (sensor.py:77-82). ru/rn: row prefixes

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MDRT_ABI_VERSION 1
+#define MDRT_ABI_VERSION 2   /* 2: link_states/link_map in mdrt_step_args, peer/bvh/query/depth_to_u8 calls */
 
 #define MDRT_OK 0
 #define MDRT_EINVAL -1   /* bad argument (shape/range/state)            */

@@ -20,6 +20,7 @@ MDRT_EINVAL = -1
 MDRT_ECUDA = -2
 MDRT_ESTATE = -3
 
+ABI_VERSION = 2            # include/mdrt.h MDRT_ABI_VERSION (StepArgs layout below)
 EARLY_TERMINATION = 0x1
 SENSOR = 0x2
 LATENCY = 0x4
@@ -162,6 +163,9 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.mdrt_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.mdrt_abi_version()}, this package needs {ABI_VERSION}: "
+                              "rebuild with `python -m paper_2602_03002_b200.build --force`")
         _lib = L
         return _lib
 

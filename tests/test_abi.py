@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_errors_without_gpu():
     L = _native.lib()
-    assert L.mdrt_abi_version() == 1
+    assert L.mdrt_abi_version() == _native.ABI_VERSION == 2
     n = _native.device_count()
     assert n >= 0
     if n == 0:

@@ -78,6 +78,23 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     """
     data = scene._new_frame(out)
     scene._guard_out(data)
+    a, keep = _pipeline_args(scene, data, sensor=sensor, step=step, frame_buffer=frame_buffer, timestamp=timestamp,
+                             delays=delays, early_termination=early_termination, clean_out=clean_out,
+                             counters=counters, rsm=rsm, rsm_modes=rsm_modes, ds_out=ds_out,
+                             downsample_factor=downsample_factor, host_ds_out=host_ds_out)
+    scene._launch(a)
+    if host_out is not None:
+        scene._deliver(data, host_out)
+    if host_ds_out is not None:
+        scene._deliver(ds_out, host_ds_out)
+    return data
+
+
+def _pipeline_args(scene: Scene, data: torch.Tensor, *, sensor, step, frame_buffer, timestamp, delays,
+                   early_termination, clean_out, counters, rsm, rsm_modes, ds_out, downsample_factor,
+                   host_ds_out):
+    """StepArgs of one render_pipeline step (advances the FrameBuffer bookkeeping);
+    returns (args, keep-alive list)."""
     a = scene._step_args(data, early_termination)
     if clean_out is not None:
         scene._new_frame(clean_out)
@@ -127,12 +144,7 @@ def render_pipeline(scene: Scene, *, sensor: SensorConfig | None = None, step: i
     if counters is not None:
         a.flags |= _native.COUNT
         a.counters = counters.data_ptr()
-    scene._launch(a)
-    if host_out is not None:
-        scene._deliver(data, host_out)
-    if host_ds_out is not None:
-        scene._deliver(ds_out, host_ds_out)
-    return data
+    return a, keep
 
 
 class CapturedStep:

@@ -487,6 +487,15 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
 #ifndef MDRT_MINB
 #define MDRT_MINB 9
 #endif
+#ifdef MDRT_TIMING
+// diagnostic build (tools/tile_times.py): per-tile start/end global timer
+__device__ unsigned long long g_tile_t0[1 << 22];
+__device__ unsigned long long g_tile_t1[1 << 22];
+extern "C" void mdrt_debug_tile_times(unsigned long long* t0, unsigned long long* t1, int n) {
+    cudaMemcpyFromSymbol(t0, g_tile_t0, sizeof(unsigned long long) * n);
+    cudaMemcpyFromSymbol(t1, g_tile_t1, sizeof(unsigned long long) * n);
+}
+#endif
 template <bool COUNT, int TW>
 static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(RenderParams p) {
     // Traversal stack in local memory: it is cached in L1 like the node
@@ -556,7 +565,19 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
             phase = (phase == 1 && nc == 0) ? 3u : (phase < 2 ? phase + 1 : phase);
         }
         if (gw == 0xffffffffu) break;
+#ifdef MDRT_TIMING
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
         render_tile<COUNT, TW>(p, gw, lane, stack);
+#ifdef MDRT_TIMING
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (lane == 0 && gw < (1u << 22)) {
+            g_tile_t0[gw] = t0;
+            g_tile_t1[gw] = t1;
+        }
+#endif
     }
 }
 

@@ -1,3 +1,9 @@
+"""Per-tile timing of one config-2 render (diagnostic): where the step's time goes
+across tiles, the tail, the slowest tiles.
+
+    python -m paper_2602_03002_b200.build --out build/libmdrt_timing.so -D MDRT_TIMING
+    python tools/tile_times.py
+"""
 import ctypes, os, sys, numpy as np, torch
 sys.path.insert(0, os.getcwd())
 os.environ["MDRT_LIB"] = "build/libmdrt_timing.so"

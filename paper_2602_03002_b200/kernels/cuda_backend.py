@@ -90,8 +90,20 @@ def _dev(x, device, slot=0):
     return stage.to(device, non_blocking=True)
 
 
+_call_lock = threading.Lock()   # the staging buffers are shared: one render_batch at a time
+
+
 def render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,
                  early_termination, out, threads=None):
+    """Reference seam (numba_backend.py:222-234); concurrent calls are serialised
+    (the reference's bindings contract is single-owner)."""
+    with _call_lock:
+        return _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,
+                             early_termination, out)
+
+
+def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,
+                  early_termination, out):
     n, c, h, w = out.shape
     device = out.device if isinstance(out, torch.Tensor) and out.is_cuda else _cuda_device(None)
     d_max = np.broadcast_to(np.asarray(d_max, np.float64), (c,))

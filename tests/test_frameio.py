@@ -97,3 +97,19 @@ def test_cuda_frames_and_async_writer(pkg, fio, tmp_path):
         paths = [w.submit(f) for f in frames]
     for path, f in zip(paths, frames):
         assert np.array_equal(pkg.read_frames(path), f.cpu().numpy())
+
+
+def test_frame_writer_host_arrays_and_errors(tmp_path, fio):
+    """FrameWriter with host arrays (no GPU): files in order, errors surface on close."""
+    frames = [fio["depth"] * (k + 1) for k in range(4)]
+    with frameio.FrameWriter(tmp_path / "seq", pattern="f_{:02d}.mdpt", depth=2) as w:
+        paths = [w.submit(f) for f in frames]
+    assert [os.path.basename(p) for p in paths] == [f"f_{k:02d}.mdpt" for k in range(4)]
+    for p, f in zip(paths, frames):
+        assert np.array_equal(frameio.read_frames(p), f.astype(np.float32))
+    w2 = frameio.FrameWriter(tmp_path / "bad")
+    w2.submit(np.zeros((2, 3)))          # not (N, C, H, W): the writer thread fails
+    with pytest.raises(ValueError):
+        w2.close()
+    with pytest.raises(ValueError):
+        frameio.FrameWriter(tmp_path, depth=0)

@@ -432,10 +432,53 @@ def render(scene: Scene, *, early_termination: bool = True, backend: str | None 
     return DepthFrame(data, timestamp)
 
 
-def render_naive_baseline(*args, **kwargs):
-    """The reference's refit-per-env baseline (scene.py:351-378) exists only
-    to be slow; the GPU renderer has no refit path to compare against."""
-    raise NotImplementedError("render_naive_baseline is a CPU benchmark foil; not provided on the GPU")
+class _FlatTris:
+    """The FlatGeometry fields the CUDA seam reads (scene.py:49-78)."""
+
+    def __init__(self, body_tris, terrain_tris):
+        empty = np.zeros((0, 3))
+        cat = (lambda k: np.concatenate([t[:, k] for t in body_tris])) if body_tris else (lambda k: empty)
+        self.tri_v0, self.tri_v1, self.tri_v2 = cat(0), cat(1), cat(2)
+        self.body_tri_offsets = np.cumsum([0] + [len(t) for t in body_tris])
+        self.body_root = np.zeros(len(body_tris), np.int32)
+        g = terrain_tris if terrain_tris is not None else np.zeros((0, 3, 3))
+        self.g_tri_v0, self.g_tri_v1, self.g_tri_v2 = g[:, 0], g[:, 1], g[:, 2]
+
+
+def render_naive_baseline(scene: Scene, *, early_termination: bool = True, backend: str | None = None,
+                          threads: int | None = None, timestamp: float = 0.0) -> DepthFrame:
+    """The reference's refit path (scene.py:351-378), kept as its comparison foil:
+    per environment every link mesh is transformed to world coordinates and gets
+    freshly built BVHs, queried with identity poses through the backend seam. The
+    terrain (static in both paths) is traced once for all envs and the closest
+    hit of the two kept. Output matches ``render`` to float32 precision; its cost
+    (host BVH builds per env and link) does not."""
+    _check_backend(backend, threads)
+    from .kernels import cuda_backend
+    n, c = scene.num_envs, scene.num_cameras
+    cam_pos, cam_rot = scene.camera_world_poses()
+    dirs, scale = scene.ray_grids()
+    d_max = scene.d_max_per_camera
+    out = torch.full(scene.frame_shape, 0.0, dtype=torch.float32, device=scene.device)
+    shared = dirs.shape[0] == 1
+    if scene.terrain is not None:
+        flat_t = _FlatTris([], scene.terrain.triangles())
+        cuda_backend.render_batch(flat_t, np.zeros((n, 0, 3)), np.zeros((n, 0, 4)), cam_pos, cam_rot, dirs, scale,
+                                  d_max, early_termination, out)
+    else:
+        out[:] = torch.as_tensor(np.asarray(d_max, np.float32), device=scene.device).view(1, c, 1, 1)
+    if scene.num_bodies:
+        bp, bq = scene._host_poses()
+        nb = scene.num_bodies
+        id_pos, id_rot = np.zeros((1, nb, 3)), np.tile(quat_identity(), (1, nb, 1))
+        part = torch.empty((1,) + scene.frame_shape[1:], dtype=torch.float32, device=scene.device)
+        for e in range(n):
+            world = [b.mesh.transformed(RigidPose(bp[e, k], bq[e, k])).triangles() for k, b in enumerate(scene.bodies)]
+            er = 0 if shared else e
+            cuda_backend.render_batch(_FlatTris(world, None), id_pos, id_rot, cam_pos[e:e + 1], cam_rot[e:e + 1],
+                                      dirs[er:er + 1], scale[er:er + 1], d_max, early_termination, part)
+            torch.minimum(out[e:e + 1], part, out=out[e:e + 1])
+    return DepthFrame(out, timestamp)
 
 
 def depth_to_z(frame, scale):

@@ -89,5 +89,22 @@ def test_backend_threads_and_out_contract(pkg):
                 torch.empty((2, 1, 9, 7), device="cuda").transpose(2, 3)):
         with pytest.raises(ValueError):
             pkg.render(scene, out=bad)
-    with pytest.raises(NotImplementedError):
-        pkg.render_naive_baseline(scene)
+
+
+def test_naive_baseline_matches_render(pkg):
+    """render_naive_baseline (scene.py:351-378: world-space link BVHs rebuilt per env)
+    equals render() to float32 precision (test_acceptance.py criterion 2's premise)."""
+    rng = np.random.default_rng(21)
+    cams = [pkg.CameraModel(width=24, height=16, hfov_deg=80.0, vfov_deg=60.0, d_max=6.0,
+                            mount=pkg.look_at_pose([2.5 * np.cos(a), 2.5 * np.sin(a), 1.5], [0.0, 0.0, 0.3]))
+            for a in (0.3, 2.4)]
+    scene = pkg.Scene(3, bodies=[("a", pkg.make_icosphere(0.3, 1)), ("b", pkg.make_box(size=(0.5, 0.3, 0.2)))],
+                      cameras=cams, terrain=pkg.make_plane(size=(8.0, 8.0)))
+    scene.set_body_poses(rng.uniform(-0.8, 0.8, size=(3, 2, 3)) * [1, 1, 0.3] + [0, 0, 0.4],
+                         rng.standard_normal((3, 2, 4)))
+    scene.set_camera_randomization(*pkg.sample_camera_offsets(pkg.CameraRandomization(seed=2), 3, 2))
+    fast = pkg.render(scene, timestamp=1.5)
+    naive = pkg.render_naive_baseline(scene, timestamp=1.5)
+    assert naive.timestamp == 1.5 and naive.shape == fast.shape
+    d = torch.abs(naive.data - fast.data)
+    assert float(d.max()) < 1e-4 and int((d > 1e-5).sum()) <= 2

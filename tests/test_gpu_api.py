@@ -108,3 +108,31 @@ def test_naive_baseline_matches_render(pkg):
     assert naive.timestamp == 1.5 and naive.shape == fast.shape
     d = torch.abs(naive.data - fast.data)
     assert float(d.max()) < 1e-4 and int((d > 1e-5).sum()) <= 2
+
+
+def test_optimized_beats_naive_refit(pkg):
+    """test_acceptance.py:106-126 (criterion 2): the no-refit render is >= 2x the
+    refit baseline on 32 envs x 2 cams with 8 bodies (here by orders of magnitude)."""
+    import time
+    rng = np.random.default_rng(5)
+    bodies = [(f"b{k}", pkg.make_icosphere(0.15, 2)) for k in range(8)]
+    cams = [pkg.CameraModel(width=64, height=36, hfov_deg=80.0, vfov_deg=55.0, d_max=6.0,
+                            mount=pkg.look_at_pose([3.0 * np.cos(a), 3.0 * np.sin(a), 1.2], [0.0, 0.0, 0.3]))
+            for a in (0.0, 3.0)]
+    scene = pkg.Scene(32, bodies=bodies, cameras=cams, terrain=pkg.make_plane(size=(8.0, 8.0)))
+    scene.set_body_poses(rng.uniform(-1, 1, size=(32, 8, 3)) * [1, 1, 0.3] + [0, 0, 0.5],
+                         rng.standard_normal((32, 8, 4)))
+    pkg.render(scene)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        pkg.render(scene)
+    torch.cuda.synchronize()
+    fast = (time.perf_counter() - t0) / 5
+    t0 = time.perf_counter()
+    naive = pkg.render_naive_baseline(scene)
+    torch.cuda.synchronize()
+    slow = time.perf_counter() - t0
+    assert torch.max(torch.abs(naive.data - pkg.render(scene).data)).item() < 1e-4
+    print(f"optimized {fast * 1e3:.2f} ms, naive refit {slow * 1e3:.1f} ms ({slow / fast:.0f}x)")
+    assert slow >= 2.0 * fast

@@ -455,6 +455,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);
         rp.tris = reinterpret_cast<const float4*>(ctx->tris.ptr);
         rp.tri_tex = ctx->triangle_texture();
+        for (int i = 0; i < 512; ++i) rp.cmix[i] = counter_mix(static_cast<unsigned long long>(i));
         rp.views = ctx->views.ptr;
         rp.links = ctx->links.ptr;
         rp.rects = ctx->rects.ptr;

@@ -192,10 +192,9 @@ __device__ __forceinline__ double normal_from_hash(unsigned long long h) {
 
 // apply_noise_dropout for one pixel (sensor.py:77-82). ru/rn: row prefixes
 // absorb(.., row); x: column counter.
-__device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru, unsigned long long rn,
-                                              unsigned long long x, double noise_scale, double dropout_p,
-                                              double fill, double dmax) {
-    const unsigned long long cx = counter_mix(x);
+__device__ __forceinline__ float sensor_apply_cx(float depth, unsigned long long ru, unsigned long long rn,
+                                                 unsigned long long cx, double noise_scale, double dropout_p,
+                                                 double fill, double dmax) {
     const bool drop = unit53(mix64(ru ^ cx)) < dropout_p;
     const double g = normal_from_hash(mix64(rn ^ cx));
     double v = __dmul_rn(static_cast<double>(depth), __dadd_rn(1.0, __dmul_rn(noise_scale, g)));
@@ -203,6 +202,12 @@ __device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru
     v = v > 1e-6 ? v : 1e-6;       // np.clip lower (DEPTH_FLOOR, sensor.py:35)
     v = v < dmax ? v : dmax;       // np.clip upper
     return static_cast<float>(v);
+}
+
+__device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru, unsigned long long rn,
+                                              unsigned long long x, double noise_scale, double dropout_p,
+                                              double fill, double dmax) {
+    return sensor_apply_cx(depth, ru, rn, counter_mix(x), noise_scale, dropout_p, fill, dmax);
 }
 
 // ---------------------------------------------------------------------------

@@ -437,14 +437,17 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     if (p.sensor) {
         // a few lanes hash the tile's rows of the uniform and of the normal stream;
         // everyone picks its row's prefixes by shuffle
-        // (lanes 0..kTileH-1: uniform stream rows, kTileH..2*kTileH-1: normal stream rows)
+        // (lanes 0..kTileH-1: uniform stream rows, kTileH..2*kTileH-1: normal stream rows).
+        // counter_mix of the row and column counters comes from a 512-entry table in
+        // the kernel parameters (constant bank) instead of one mix64 each.
         const int hl = lane % (2 * kTileH);
-        const unsigned long long rowh = absorb(hl >= kTileH ? V.hn : V.hu,
-                                               static_cast<unsigned long long>(ty * kTileH + hl % kTileH));
+        const uint32_t rrow = ty * kTileH + hl % kTileH;
+        const unsigned long long rowh = mix64((hl >= kTileH ? V.hn : V.hu) ^
+                                              (rrow < 512 ? p.cmix[rrow] : counter_mix(rrow)));
         const unsigned long long ru = __shfl_sync(0xffffffffu, rowh, lane / kTileW);
         const unsigned long long rn = __shfl_sync(0xffffffffu, rowh, kTileH + lane / kTileW);
-        val = sensor_apply(z, ru, rn, static_cast<unsigned long long>(px), p.noise_scale, p.dropout_p,
-                           p.fill[c], p.dmax64[c]);
+        const unsigned long long cx = px < 512 ? p.cmix[px] : counter_mix(static_cast<unsigned long long>(px));
+        val = sensor_apply_cx(z, ru, rn, cx, p.noise_scale, p.dropout_p, p.fill[c], p.dmax64[c]);
     }
     if (active) {
         const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;

@@ -101,6 +101,7 @@ struct RenderParams {
     int32_t rsm;                  // apply side masking to the observation
     double rsm_low;
     double rsm_high[64];
+    unsigned long long cmix[512];  // counter_mix(v) for v < 512 (rows and columns of the RNG counters)
 };
 
 struct NoiseParams {

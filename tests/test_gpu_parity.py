@@ -476,3 +476,38 @@ def test_bound_link_states_zero_copy(pkg):
         s_bind.bind_link_states(wx, lmap, rot_offset=8)
     s_bind.set_body_poses(case["body_pos"], case["body_rot"])            # unbinds
     assert torch.equal(pkg.render(s_bind).data, pkg.render(s_ref).data)
+
+
+def test_captured_full_pipeline_equals_eager(pkg):
+    """Everything at once (sensor + latency ring + side masking + fused 5x5 downsample),
+    eager vs CUDA-graph replay, bitwise, over several steps."""
+    from paper_2602_03002_b200.pipeline import CapturedStep
+    cam = pkg.CameraModel(width=60, height=45, hfov_deg=87.0, vfov_deg=58.0, d_max=6.0,
+                          mount=pkg.look_at_pose([0.0, 0.0, 1.2], [1.5, 0.3, 0.0]))
+    xs = np.linspace(-4, 4, 41)
+    gx, gy = np.meshgrid(xs, xs)
+    a = (np.arange(40)[:, None] * 41 + np.arange(40)[None, :]).ravel()
+    faces = np.concatenate([np.column_stack([a, a + 1, a + 42]), np.column_stack([a, a + 42, a + 41])])
+    terrain = pkg.TriMesh(np.column_stack([gx.ravel(), gy.ravel(), 0.2 * np.sin(2 * gx.ravel())]), faces)
+    scenes = [pkg.Scene(5, bodies=[("box", pkg.make_box(size=(0.3, 0.3, 0.3)))], cameras=[cam, cam],
+                        terrain=terrain) for _ in range(2)]
+    rng = np.random.default_rng(3)
+    sens_cfg = pkg.SensorConfig(seed=4)
+    rsm = pkg.RsmConfig(seed=5)
+    modes = pkg.rsm_sample_modes(rsm, "stepping_stones", 5, 2, episode=0)
+    delays = np.array([0.0, 0.02, 0.05, 0.1, 0.03])
+    fb_e, fb_g = pkg.FrameBuffer(capacity=4), pkg.FrameBuffer(capacity=4)
+    ds_e, ds_g = (torch.empty((5, 2, 9, 12), device="cuda") for _ in range(2))
+    cap = CapturedStep(scenes[1], sensor=sens_cfg, frame_buffer=fb_g, delays=delays, dt=0.02, first_step=0,
+                       rsm=rsm, rsm_modes=modes, ds_out=ds_g)
+    for k in range(6):
+        pos = rng.uniform(-1, 1, size=(5, 1, 3)) * [1, 1, 0.2] + [1.2, 0, 0.5]
+        rot = rng.standard_normal((5, 1, 4))
+        for sc in scenes:
+            sc.set_body_poses(pos, rot)
+        eager = pkg.render_pipeline(scenes[0], sensor=sens_cfg, step=k, frame_buffer=fb_e, timestamp=0.02 * k,
+                                    delays=delays, rsm=rsm, rsm_modes=modes, ds_out=ds_e).clone()
+        graph = cap.replay()
+        assert torch.equal(graph, eager), f"obs step {k}"
+        assert torch.equal(ds_g, ds_e), f"downsample step {k}"
+        assert torch.equal(ds_e, pkg.downsample_min(eager, 5))

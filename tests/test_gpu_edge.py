@@ -6,6 +6,7 @@ with different ranges, parented cameras on a moving link.
 """
 
 import numpy as np
+import torch
 import pytest
 
 from test_gpu_acceptance import f32, random_scene
@@ -135,3 +136,32 @@ def test_high_resolution_camera(pkg, oracle):
     hi = pkg.CameraModel(width=320, height=240, hfov_deg=cam.hfov_deg, vfov_deg=cam.vfov_deg, d_max=cam.d_max,
                          mount=cam.mount)
     _check(pkg, oracle, bodies, terrain, [hi], pos, rot, 2, max_bad=int(1e-4 * 2 * 320 * 240) + 1)
+
+
+def test_two_scenes_alternating(pkg, oracle):
+    """Two live scenes with different image widths (4x8 and 8x4 tiles, separate
+    native contexts) rendered alternately stay independent and match the oracle."""
+    g = np.random.default_rng(12)
+    bodies, terrain, cams, pos, rot, _ = random_scene(pkg, g, num_envs=2, num_cams=1, num_bodies=4)
+    cam = cams[0]
+    narrow = pkg.CameraModel(width=48, height=32, hfov_deg=cam.hfov_deg, vfov_deg=cam.vfov_deg,
+                             d_max=cam.d_max, mount=cam.mount)
+    wide = pkg.CameraModel(width=160, height=96, hfov_deg=cam.hfov_deg, vfov_deg=cam.vfov_deg,
+                           d_max=cam.d_max, mount=cam.mount)
+    sa = pkg.Scene(2, bodies=[(f"b{k}", m) for k, m in enumerate(bodies)], cameras=[narrow], terrain=terrain)
+    sb = pkg.Scene(2, bodies=[(f"b{k}", m) for k, m in enumerate(bodies)], cameras=[wide], terrain=terrain)
+    for s in (sa, sb):
+        s.set_body_poses(pos, rot)
+    first = [pkg.render(sa).data.clone(), pkg.render(sb).data.clone()]
+    for _ in range(3):
+        assert torch.equal(pkg.render(sb).data, first[1])
+        assert torch.equal(pkg.render(sa).data, first[0])
+    for s, out in ((sa, first[0]), (sb, first[1])):
+        c = s.cameras[0]
+        osc = oracle.OracleScene([(m.vertices, m.faces) for m in bodies], (terrain.vertices, terrain.faces),
+                                 [dict(width=c.width, height=c.height, hfov_deg=c.hfov_deg, vfov_deg=c.vfov_deg,
+                                       d_max=c.d_max, mount_pos=c.mount.translation, mount_rot=c.mount.rotation,
+                                       parent=None)])
+        ref = osc.render(pos, rot)
+        d = np.abs(out.cpu().numpy().astype(np.float64) - ref)
+        assert int((d > 1e-4).sum()) <= max(1, int(1e-4 * d.size))

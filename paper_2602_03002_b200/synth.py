@@ -6,7 +6,10 @@ the named shapes:
 
 * terrain: 0.05 m height-grid tiles (slope pyramid, stairs up/down, rolling),
   stepping stones as boxes over a recessed floor -- same construction rules as
-  terrain.py:218-360 (grid meshes, box stones), re-derived here;
+  terrain.py:218-360 (grid meshes, box stones), re-derived here; the config 1,
+  2 and 3 meshes equal the reference generator's bit for bit (stairs tiles
+  centred in their 6 m tile: x shifted by 1.08 m), pinned by
+  tests/test_host_api.py against checksums written by the live reference;
 * G1 proxy: 30 rigid links (pelvis, 2x6 leg, 3 waist, 2x7 arm) meshed as
   ellipsoids/boxes in their link frames (~8.7k triangles), posed by forward
   kinematics with per-step joint perturbations from the counter RNG stream

@@ -154,10 +154,33 @@ def make_frameio(md):
     np.savez_compressed(os.path.join(HERE, "frameio.npz"), **fio)
 
 
+def make_terrain(md):
+    """Checksums of the reference generator's meshes for the benchmark terrains
+    (terrain.py:278-360): synth.py's tiles must reproduce them bit for bit."""
+    import hashlib
+    from multidepth.terrain import TerrainSpec, generate_terrain
+    plat = (6 - 8 * 0.27) / 2
+    specs = {"cfg1_stairs": TerrainSpec(kind="stairs_up"),
+             "tile_slope_pyramid": TerrainSpec(kind="slope_pyramid", size=(6.0, 6.0), incline_deg=20.0),
+             "tile_stairs_up": TerrainSpec(kind="stairs_up", width=6.0, platform_length=plat),
+             "tile_stairs_down": TerrainSpec(kind="stairs_down", width=6.0, platform_length=plat),
+             "cfg3_stones": TerrainSpec(kind="stepping_stones", stone_size=0.25, stone_gap=0.60, size=(24, 24))}
+    out = {}
+    shift = {"tile_stairs_up": 1.08, "tile_stairs_down": 1.08}   # stairs tiles are centred in synth.py
+    for name, spec in specs.items():
+        m, _ = generate_terrain(spec)
+        v = np.array(m.vertices, np.float64)
+        v[:, 0] -= shift.get(name, 0.0)
+        out[name + "_vsha"] = np.array(hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest())
+        out[name + "_fsha"] = np.array(hashlib.sha256(np.ascontiguousarray(m.faces, np.int64).tobytes()).hexdigest())
+        out[name + "_shape"] = np.array([len(m.vertices), len(m.faces)])
+    np.savez_compressed(os.path.join(HERE, "terrain.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=os.environ.get("MULTIDEPTH_REF", "/root/reference/pkg/src"))
-    ap.add_argument("--only", choices=["frameio"], default=None, help="regenerate one fixture group")
+    ap.add_argument("--only", choices=["frameio", "terrain"], default=None, help="regenerate one fixture group")
     args = ap.parse_args()
     os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_cache_golden"))
     sys.dont_write_bytecode = True
@@ -167,8 +190,11 @@ def main():
     from multidepth import rng as mrng
     from paper_2602_03002_b200 import synth
 
-    make_frameio(md)
-    if args.only == "frameio":
+    if args.only in (None, "frameio"):
+        make_frameio(md)
+    if args.only in (None, "terrain"):
+        make_terrain(md)
+    if args.only is not None:
         print("done")
         return
     out = {}

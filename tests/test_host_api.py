@@ -175,3 +175,24 @@ def test_rsm_host_side(sens):
         cfg.probs_for("volcano")
     with pytest.raises(ValueError):
         RsmConfig(probs={"flat": (0.5, 0.5, 0.5)})
+
+
+def test_benchmark_terrains_are_the_reference_generators():
+    """synth.py's config 1/2/3 terrains reproduce the reference generator's meshes
+    (terrain.py:278-360) bit for bit (stairs tiles up to their placement shift)."""
+    import hashlib
+    from paper_2602_03002_b200 import synth
+    ref = np.load(os.path.join(GOLDEN, "terrain.npz"))
+
+    def check(name, mesh):
+        v = np.array(mesh.vertices, np.float64)
+        assert [len(v), len(mesh.faces)] == ref[name + "_shape"].tolist()
+        assert hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() == str(ref[name + "_vsha"])
+        assert hashlib.sha256(np.ascontiguousarray(mesh.faces, np.int64).tobytes()).hexdigest() == \
+            str(ref[name + "_fsha"])
+
+    check("cfg1_stairs", synth.stairs_terrain().mesh)
+    check("tile_slope_pyramid", synth.tile_field(["slope_pyramid"]).mesh)
+    check("tile_stairs_up", synth.tile_field(["stairs_up"]).mesh)       # fixture: reference x - 1.08
+    check("tile_stairs_down", synth.tile_field(["stairs_down"]).mesh)
+    check("cfg3_stones", synth.stepping_stones().mesh)

@@ -74,9 +74,10 @@ def cfg_envs(name):
 
 def workload_desc(name):
     return {
-        "cfg2": "4096 envs x 2 cams (front+back) 64x48 per GPU, 3x3 slope/stairs tiles (259,200 tris), "
-                "30-link G1 proxy (8,060 tris), full noise/dropout/latency",
-        "cfg3": "4096 envs x 4 cams 64x48, stepping stones 25cm/60cm (8,750 tris), arms raised, full sensor",
+        "cfg2": "4096 envs x 2 cams (front+back) 64x48 per GPU, 3x3 slope/stairs tiles (259,200 tris, the reference "
+                "generate_terrain meshes), 30-link G1 proxy (8,060 tris), full noise/dropout/latency",
+        "cfg3": "4096 envs x 4 cams 64x48, stepping stones 25cm/60cm (8,750 tris, the reference generate_terrain "
+                "mesh), arms raised, full sensor",
         "cfg5": "4096 envs x 2 cams 160x120, 1300x1300-node rolling terrain (3,373,802 tris, BVH ~270 MB > 2x L2), "
                 "full sensor",
         "cfg5_1m": "4096 envs x 2 cams 160x120, 708x708-node rolling terrain (999,698 tris), full sensor",

@@ -17,6 +17,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmdrt.so")
+# diagnostic variant with device-side bounds checks (MDRT_CHECKS): load it with
+# MDRT_LIB=<path> to run any test or tool with every index checked
+LIB_CHECKED = os.path.join(HERE, "libmdrt_checked.so")
 SOURCES = ["bvh_build.cpp", "mdrt_kernels.cu", "mdrt_api.cu"]
 HEADERS = ["bvh_build.h", "mdrt_device.cuh", "mdrt_kernels.h"]
 
@@ -37,11 +40,18 @@ def _inputs() -> list[str]:
     return files
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(f) <= t for f in _inputs())
+
+
+def build_checked(force: bool = False) -> str:
+    """Compile libmdrt_checked.so (MDRT_CHECKS) unless it is up to date."""
+    if not force and up_to_date(LIB_CHECKED):
+        return LIB_CHECKED
+    return build(out=LIB_CHECKED, defines=("MDRT_CHECKS",))
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
@@ -72,5 +82,9 @@ if __name__ == "__main__":
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--checked", action="store_true", help="build libmdrt_checked.so (MDRT_CHECKS)")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose, out=a.out, defines=tuple(a.defines)))
+    if a.checked:
+        print(build_checked(force=a.force))
+    else:
+        print(build(force=a.force, verbose=a.verbose, out=a.out, defines=tuple(a.defines)))

@@ -98,6 +98,7 @@ struct mdrt_ctx {
     std::vector<PackedTree> bodies;
     PackedTree terrain;
     bool has_terrain = false;
+    int32_t node_count = 0, tri_count = 0;   // records uploaded at the last commit
     // cameras
     int32_t C = 0, W = 0, H = 0;
     std::vector<CamRig> rigs;
@@ -300,6 +301,8 @@ int mdrt_commit(mdrt_ctx* ctx) {
         ctx->drop_tri_tex();
         ctx->nodes.reserve(nodes.size());
         ctx->tris.reserve(tris.size());
+        ctx->node_count = static_cast<int32_t>(nodes.size());
+        ctx->tri_count = static_cast<int32_t>(tris.size());
         ctx->body_info.reserve(infos.size());
         ctx->rig_buf.reserve(ctx->rigs.size());
         CK(cudaMemcpy(ctx->nodes.ptr, nodes.data(), nodes.size() * sizeof(PackedNode), cudaMemcpyHostToDevice));
@@ -454,6 +457,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.terrain_root = ctx->has_terrain ? ctx->terrain_root : -1;
         rp.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);
         rp.tris = reinterpret_cast<const float4*>(ctx->tris.ptr);
+        rp.n_nodes = ctx->node_count;
+        rp.n_tris = ctx->tri_count;
         rp.tri_tex = ctx->triangle_texture();
         for (int i = 0; i < 512; ++i) rp.cmix[i] = counter_mix(static_cast<unsigned long long>(i));
         rp.views = ctx->views.ptr;
@@ -471,6 +476,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         }
         rp.ring = latency ? a->ring : nullptr;
         rp.write_slot = a->write_slot;
+        rp.ring_slots = a->ring_slots;
         rp.out_clean = a->out_clean;
         rp.out = a->out;
         rp.counters = a->counters;
@@ -692,6 +698,7 @@ int mdrt_query_rays(const void* nodes, const void* tris, const float* origins, c
         QueryParams q{};
         q.nodes = static_cast<const float4*>(nodes);
         q.tris = static_cast<const float4*>(tris);
+        q.n_nodes = q.n_tris = INT32_MAX;   // the ABI passes no record counts
         q.root = 0;
         q.origins = origins;
         q.dirs = dirs;

@@ -7,10 +7,29 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace mdrt {
+
+// MDRT_CHECKS (diagnostic build, tools/checked_build.py): device-side bounds
+// checks on every node/triangle/stack/output index; a violated check prints the
+// offending values and traps, so the launch fails with an error instead of
+// reading or writing out of range. Release builds compile the checks away.
+#ifdef MDRT_CHECKS
+#define MDRT_CHECK(cond, fmt, ...)                                                         \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("MDRT_CHECK %s:%d %s: " fmt "\n", __FILE__, __LINE__, #cond, __VA_ARGS__); \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#define MDRT_SET_LIMITS(tv, n, t) ((tv).lim_nodes = (n), (tv).lim_tris = (t))
+#else
+#define MDRT_CHECK(cond, fmt, ...) ((void)0)
+#define MDRT_SET_LIMITS(tv, n, t) ((void)(n), (void)(t))
+#endif
 
 constexpr int kStack = 24;          // == kMaxDepth of the builder
 #ifndef MDRT_BLOCK
@@ -271,6 +290,9 @@ struct Traversal {
     int32_t ref;
     int2* top;
     int2* bottom;
+#ifdef MDRT_CHECKS
+    int32_t lim_nodes, lim_tris;   // record counts of the node / triangle buffers
+#endif
 
     __device__ __forceinline__ void init(int32_t root, float ox_, float oy_, float oz_, float dx_, float dy_,
                                          float dz_, float tmax, int2* stack) {
@@ -290,6 +312,7 @@ struct Traversal {
     }
 
     __device__ __forceinline__ void push(int2 e) {
+        MDRT_CHECK((top - bottom) / kStackStride < kStack, "stack depth %d", static_cast<int>((top - bottom) / kStackStride));
         *top = e;
         top += kStackStride;
     }
@@ -310,6 +333,7 @@ struct Traversal {
         const int32_t v = ~lref;
         const int32_t first = v >> 3;
         const int32_t cnt = (v & 7) + 1;
+        MDRT_CHECK(first >= 0 && first + cnt <= lim_tris, "leaf first %d count %d of %d triangles", first, cnt, lim_tris);
         for (int32_t i = 0; i < cnt; ++i) {
             float4 v0, e1, e2;
             if constexpr (TEXTRI) {
@@ -356,6 +380,7 @@ struct Traversal {
     template <int OCT>
     __device__ __forceinline__ void descend_t(const float4* __restrict__ nodes, TraceCounters& ctr) {
         while (ref >= 0) {
+            MDRT_CHECK(ref < lim_nodes, "node %d of %d", ref, lim_nodes);
             const float4* n = nodes + 4 * static_cast<int64_t>(ref);
             float4 bx, by, bz, rff;
             ldg256(n, bx, by);        // c0 x lo/hi, c0 y lo/hi | c1 x lo/hi, c1 y lo/hi
@@ -427,9 +452,10 @@ template <bool COUNT>
 __device__ __forceinline__ float trace(const float4* __restrict__ nodes, cudaTextureObject_t tri_tex,
                                        int32_t root, float ox, float oy, float oz, float dx, float dy,
                                        float dz, float tmax, int2* __restrict__ stack,
-                                       TraceCounters& ctr) {
+                                       TraceCounters& ctr, int32_t lim_nodes, int32_t lim_tris) {
     Traversal<COUNT, false, true> tv;
     tv.init(root, ox, oy, oz, dx, dy, dz, tmax, stack);
+    MDRT_SET_LIMITS(tv, lim_nodes, lim_tris);
     tv.tri_tex = tri_tex;
     const float4* tris = nullptr;   // triangles come from tri_tex
     while (!tv.round(nodes, tris, ctr)) {
@@ -444,9 +470,10 @@ template <bool COUNT>
 __device__ __forceinline__ float trace_oct(const float4* __restrict__ nodes, cudaTextureObject_t tri_tex,
                                            int32_t root, float ox, float oy, float oz, float dx, float dy,
                                            float dz, float tmax, int2* __restrict__ stack,
-                                           TraceCounters& ctr) {
+                                           TraceCounters& ctr, int32_t lim_nodes, int32_t lim_tris) {
     Traversal<COUNT, false, true> tv;
     tv.init(root, ox, oy, oz, dx, dy, dz, tmax, stack);
+    MDRT_SET_LIMITS(tv, lim_nodes, lim_tris);
     tv.tri_tex = tri_tex;
     const float4* tris = nullptr;   // triangles come from tri_tex
     const int oct = tv.octant();

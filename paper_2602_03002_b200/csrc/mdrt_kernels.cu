@@ -63,6 +63,8 @@ __device__ __forceinline__ void qmat(Q q, double m[9]) {
 // a simulator's link-state tensor (zero-copy ingestion), quaternion as wxyz.
 __device__ __forceinline__ void load_pose(const PrologueParams& p, int64_t e, int b, float t[3], float q[4]) {
     if (p.link_states) {
+        MDRT_CHECK(p.link_map[b] >= 0 && p.link_map[b] < p.env_stride, "body %d maps to link %d of %lld", b,
+                   p.link_map[b], static_cast<long long>(p.env_stride));
         const float* r = p.link_states + (e * p.env_stride + p.link_map[b]) * p.record_stride;
         t[0] = r[p.pos_offset]; t[1] = r[p.pos_offset + 1]; t[2] = r[p.pos_offset + 2];
         const float* qq = r + p.rot_offset;
@@ -292,6 +294,7 @@ static __global__ void __launch_bounds__(128, MDRT_PRO_MINB) prologue_kernel(Pro
                 else lo = mid + 1;
             }
             const int kk = lo - 1 < 0 ? 0 : lo - 1;
+            MDRT_CHECK(count >= 0 && count <= 32 && kk < 32, "ring count %d index %d", count, kk);
             const int slot = order[kk];
             v.read_slot = slot == wslot ? -1 : slot;
             if (c == 0 && p.read_slot_out) p.read_slot_out[e] = slot;
@@ -331,11 +334,14 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     const bool active = px < p.W && py < p.H;
     const uint32_t e = fast_div(view, static_cast<uint32_t>(p.C), p.m_C);
     const uint32_t c = view - e * static_cast<uint32_t>(p.C);
+    MDRT_CHECK(view < static_cast<uint32_t>(p.N * p.C) && e < static_cast<uint32_t>(p.N) && tx < static_cast<uint32_t>(p.tiles_x),
+               "tile %u: view %u env %u tx %u", gw, view, e, tx);
 
     const ViewRec& V = p.views[view];
     const float4 in = *reinterpret_cast<const float4*>(&V.ax);     // ax bx ay by
     const float dmax = V.dmax;
     const int nlinks = V.nlinks;
+    MDRT_CHECK(nlinks >= 0 && nlinks <= p.B, "view %u nlinks %d of %d", view, nlinks, p.B);
 
     // camera-frame direction and scale (camera.py:81-90)
     float dcx, dcy, dcz, m;
@@ -392,7 +398,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
                 const float bound = p.early_termination ? z : dmax;
                 const unsigned int before = ctr.nodes;
                 const float tt = trace<COUNT>(p.nodes, p.tri_tex, L.root, m2.y, m2.z, m2.w, ldx, ldy, ldz,
-                                              bound * inv_m, stack, ctr);
+                                              bound * inv_m, stack, ctr, p.n_nodes, p.n_tris);
                 if (COUNT) {
                     ctr.link_nodes += ctr.nodes - before;
                     ++ctr.link_traces;
@@ -414,10 +420,10 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const float bound = p.early_termination ? z : dmax;
 #ifdef MDRT_NO_OCTANT
         const float tt = trace<COUNT>(p.nodes, p.tri_tex, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
-                                      bound * inv_m, stack, ctr);
+                                      bound * inv_m, stack, ctr, p.n_nodes, p.n_tris);
 #else
         const float tt = trace_oct<COUNT>(p.nodes, p.tri_tex, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
-                                          bound * inv_m, stack, ctr);
+                                          bound * inv_m, stack, ctr, p.n_nodes, p.n_tris);
 #endif
         const float cand = m * tt;
         if (cand < z) z = cand;
@@ -452,6 +458,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
     if (active) {
         const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
         if (p.out_clean) st_stream(p.out_clean + o, z);
+        MDRT_CHECK(o >= 0 && o < static_cast<int64_t>(p.N) * p.C * p.H * p.W, "pixel index %lld", static_cast<long long>(o));
         if (p.ring) {
             // ring traffic streams past L1/L2 (evict-first) so it does not
             // displace BVH records; a zero-lag read is the value just written
@@ -459,6 +466,8 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
             const int wslot = p.state ? p.state->write_slot : p.write_slot;
             st_stream(p.ring + static_cast<int64_t>(wslot) * frame + o, val);
             const int rs = V.read_slot;
+            MDRT_CHECK(wslot >= 0 && wslot < p.ring_slots && rs < p.ring_slots, "ring slots write %d read %d of %d",
+                       wslot, rs, p.ring_slots);
             if (rs >= 0 && rs != wslot) val = __ldcs(p.ring + static_cast<int64_t>(rs) * frame + o);
         }
         if (p.rsm) {
@@ -479,6 +488,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const int f = p.ds_factor;
         const long long key = active ? (static_cast<long long>(view) * p.ds_h + py / f) * p.ds_w + px / f
                                      : -1LL - lane;
+        MDRT_CHECK(!active || key < static_cast<long long>(p.N) * p.C * p.ds_h * p.ds_w, "ds index %lld", key);
         const unsigned grp = __match_any_sync(0xffffffffu, key);
         const unsigned mn = __reduce_min_sync(grp, __float_as_uint(val));
         if (active && lane == __ffs(grp) - 1) atomicMin(p.ds_out + key, mn);
@@ -703,6 +713,7 @@ static __global__ void __launch_bounds__(128) query_kernel(QueryParams p) {
     Traversal<false, true> tv;
     tv.init(p.root, p.origins[3 * i], p.origins[3 * i + 1], p.origins[3 * i + 2], p.dirs[3 * i], p.dirs[3 * i + 1],
             p.dirs[3 * i + 2], p.t_max, stack);
+    MDRT_SET_LIMITS(tv, p.n_nodes, p.n_tris);
     while (!tv.round(p.nodes, p.tris, ctr)) {
     }
     p.t_out[i] = tv.result();

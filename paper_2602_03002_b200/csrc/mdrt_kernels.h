@@ -74,6 +74,7 @@ struct RenderParams {
     int32_t terrain_root;
     const float4* nodes;
     const float4* tris;
+    int32_t n_nodes, n_tris;      // record counts (bounds of the MDRT_CHECKS build)
     cudaTextureObject_t tri_tex;  // texture object over `tris` (float4 texels): the traversal reads triangles here
     const ViewRec* views;
     const LinkRec* links;
@@ -87,6 +88,7 @@ struct RenderParams {
     double dmax64[64];
     float* ring;
     int32_t write_slot;
+    int32_t ring_slots;           // frames in `ring` (bounds of the MDRT_CHECKS build)
     float* out_clean;
     float* out;
     unsigned long long* counters;
@@ -159,6 +161,7 @@ void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s);
 struct QueryParams {
     const float4* nodes;
     const float4* tris;
+    int32_t n_nodes, n_tris;
     int32_t root;
     const float* origins;   // (n, 3)
     const float* dirs;      // (n, 3)

@@ -453,6 +453,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.m_tiles_x = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_x));
         rp.m_tiles_per_view = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_per_view));
         rp.m_C = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(C));
+        rp.row_tiles = static_cast<uint32_t>(N) * static_cast<uint32_t>(C) * static_cast<uint32_t>(rp.tiles_x);
+        rp.m_row_tiles = static_cast<uint32_t>(0xffffffffu / rp.row_tiles);
         rp.early_termination = (a->flags & MDRT_EARLY_TERMINATION) != 0;
         rp.terrain_root = ctx->has_terrain ? ctx->terrain_root : -1;
         rp.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);

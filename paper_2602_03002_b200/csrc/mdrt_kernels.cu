@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 namespace mdrt {
 
@@ -325,10 +326,16 @@ template <bool COUNT, int TW>
 __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, int lane, int2* stack) {
     constexpr int kTileW = TW;          // this launch's tile shape: TW x (32 / TW) pixels
     constexpr int kTileH = 32 / TW;
-    const uint32_t view = fast_div(gw, static_cast<uint32_t>(p.tiles_per_view), p.m_tiles_per_view);
-    const uint32_t tile = gw - view * static_cast<uint32_t>(p.tiles_per_view);
-    const uint32_t ty = fast_div(tile, static_cast<uint32_t>(p.tiles_x), p.m_tiles_x);
-    const uint32_t tx = tile - ty * static_cast<uint32_t>(p.tiles_x);
+    // gw -> (q1, q2, tx) by two mixed-radix divisions; view-major order has
+    // q1 = view, q2 = tile row, tile-row-major order (row_order) the reverse:
+    // tile row 0 of every view comes first, so the expensive rows (towards
+    // the horizon) start early and the launch ends on cheap near-ground rows
+    const uint32_t q1 = fast_div(gw, p.order_d1, p.order_m1);
+    const uint32_t r1 = gw - q1 * p.order_d1;
+    const uint32_t q2 = fast_div(r1, static_cast<uint32_t>(p.tiles_x), p.m_tiles_x);
+    const uint32_t tx = r1 - q2 * static_cast<uint32_t>(p.tiles_x);
+    const uint32_t view = p.row_order ? q2 : q1;
+    const uint32_t ty = p.row_order ? q1 : q2;
     const int px = static_cast<int>(tx) * kTileW + (lane & (kTileW - 1));
     const int py = static_cast<int>(ty) * kTileH + lane / kTileW;
     const bool active = px < p.W && py < p.H;
@@ -844,6 +851,21 @@ static void launch_render_tw(const RenderParams& p, int64_t warps, bool count, i
             q.chunks = 0;
             q.local_tiles = 0;
         }
+        // Tile order: tile-row-major over all views unless the tiles are
+        // scheduled SM-locally (there view-major chunks keep an SM on the same
+        // envs' geometry). The last ~0.1 ms of a view-major launch is a few
+        // horizon-row tiles costing ~20x the mean (tools/tile_times.py); taking
+        // every view's top rows first ends the launch on cheap rows: config 2
+        // +3.0 %, paper +1.1 %, config 3 +-0 (config 5 view-major: row-major
+        // would cost 6 %). MDRT_TILE_ORDER=view|row overrides.
+        static int env_order = -2;
+        if (env_order == -2) {
+            const char* o = std::getenv("MDRT_TILE_ORDER");
+            env_order = !o ? -1 : (std::strcmp(o, "row") == 0 ? 1 : 0);
+        }
+        q.row_order = env_order >= 0 ? env_order : (q.chunks == 0 ? 1 : 0);
+        q.order_d1 = q.row_order ? q.row_tiles : static_cast<uint32_t>(q.tiles_per_view);
+        q.order_m1 = q.row_order ? q.m_row_tiles : q.m_tiles_per_view;
     }
     if (count)
         render_kernel<true, TW><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(q);

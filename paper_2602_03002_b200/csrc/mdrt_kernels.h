@@ -70,6 +70,9 @@ struct RenderParams {
     int32_t tile_w;               // tile shape: tile_w x (32 / tile_w) pixels (4 or 8)
     int32_t tiles_x, tiles_per_view;
     uint32_t m_tiles_x, m_tiles_per_view, m_C;   // fast_div multipliers floor((2^32-1)/d)
+    uint32_t row_tiles, m_row_tiles;             // tiles in one tile row of all views (N * C * tiles_x)
+    int32_t row_order;            // tile index order: 1 = tile-row-major over all views, 0 = view-major
+    uint32_t order_d1, order_m1;  // first divisor of the tile decode (row_tiles or tiles_per_view) + multiplier
     int32_t early_termination;
     int32_t terrain_root;
     const float4* nodes;

@@ -7,6 +7,8 @@ python tools/launch_summary.py gpurun_out/$TAG/launches.csv "python bench.py --s
 cp gpurun_out/$TAG/launches.csv profiles/r01_launches_ncu.csv
 python tools/ncu_summary.py gpurun_out/$TAG/prof_render_cfg2.ncu-rep --title "render_kernel, config 2 (4096 envs x 2 cams 64x48, full sensor + latency), round 1" > profiles/r01_render_kernel_ncu.md
 python tools/ncu_summary.py gpurun_out/$TAG/prof_render_cfg5.ncu-rep --title "render_kernel, config 5 (4096 envs x 2 cams 160x120, 3.37M-tri terrain), round 1" > profiles/r01_render_kernel_cfg5_ncu.md
+[ -f gpurun_out/$TAG/prof_render_cfg3.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$TAG/prof_render_cfg3.ncu-rep --title "render_kernel, config 3 (4096 envs x 4 cams 64x48, stepping stones), round 1" > profiles/r01_render_kernel_cfg3_ncu.md
+[ -f gpurun_out/$TAG/prof_render_paper.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$TAG/prof_render_paper.ncu-rep --title "render_kernel, paper (1024 envs x 2 cams 240x135 + fused 5x5 min-pool), round 1" > profiles/r01_render_kernel_paper_ncu.md
 cp gpurun_out/$TAG/prof_render_cfg2.ncu-rep profiles/r01_render_kernel_full.ncu-rep
 python - <<'PY'
 import json, re

@@ -570,9 +570,11 @@ def main():
         value = all_rays / (total_ms * 1e-3)
         e2e_value = all_rays / (e2e_ms * 1e-3)
         # algorithmic bytes of one render-kernel launch (this rank's slice)
-        node_b = scene.geometry_stats["node_record_size"]
+        # a node visit reads 56 of the 64 B record (boxes + child refs; the pad is not fetched)
+        node_b = scene.geometry_stats["node_record_size"] - 8
         tri_b = scene.geometry_stats["tri_record_size"]
-        warps = n * C * math.ceil(W / 8) * math.ceil(H / 4)
+        tw = int(os.environ.get("MDRT_TILE_W", "0")) or (4 if W <= 96 else 8)   # render_tile_width
+        warps = n * C * math.ceil(W / tw) * math.ceil(H / (32 // tw))
         lag_frac = float(np.mean(delays_np >= dt))    # envs reading an older ring slot
         io_b = 4 + 4 + 4 * lag_frac                   # ring write + obs write + delayed read
         bytes_per_ray = nodes_per_ray * node_b + tris_per_ray * tri_b + io_b
@@ -617,7 +619,7 @@ def main():
             "steps_per_s": 1e3 / (total_ms / args.steps),
             "per_ray": {"node_fetches": nodes_per_ray, "tri_tests": tris_per_ray, "bytes": bytes_per_ray,
                         "link_node_fetches": link_nodes_per_ray, "link_traversals": link_traces_per_ray,
-                        "node_record_b": node_b, "tri_record_b": tri_b, "io_b": io_b},
+                        "node_record_b": node_b + 8, "node_fetch_b": node_b, "tri_record_b": tri_b, "io_b": io_b},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "render_kernel (K1+K2+K3 fused)", "kernel_ms": kernel_ms,

@@ -1,7 +1,7 @@
 // Host-side BVH construction and packing for the B200 renderer.
 //
 // Replaces the reference's per-mesh build (bvh.py:68-136, a median split with
-// leaf <= 4 and f64 flat arrays) with a binned-SAH build whose output is packed
+// leaf <= 4 and f64 flat arrays) with an SAH build (32 bins, exact sweep below 1024 triangles) whose output is packed
 // for the GPU: every inner node is one 64-byte record holding BOTH children's
 // fp32 boxes (so one record fetch tests two boxes) and triangles are 48-byte
 // {v0, e1, e2} records. Boxes are padded outward so fp32 slab tests stay

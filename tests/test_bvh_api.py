@@ -109,3 +109,38 @@ def test_query_t_max_single_ray_and_cuda_batch():
     assert tt.is_cuda and ff.dtype == torch.int32
     assert tt[0].item() == pytest.approx(4.5) and np.isinf(tt[1].item()) and ff[1].item() == -1
     assert tt[2].item() == pytest.approx(0.5)      # from inside: double-sided wall hit
+
+
+_SAH_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+from paper_2602_03002_b200 import bvh as B
+from test_bvh_api import random_mesh
+mesh = random_mesh(np.random.default_rng(11), num_tris=3000, spread=6.0)
+b = B.build_bvh(mesh)
+B.validate_bvh(b, mesh)
+# SAH cost of the tree (node cost 1.2, triangle cost 1), relative to the root box
+area = lambda lo, hi: 2 * ((hi - lo)[:, 0] * (hi - lo)[:, 1] + (hi - lo)[:, 1] * (hi - lo)[:, 2] + (hi - lo)[:, 2] * (hi - lo)[:, 0])
+a = area(b.node_min, b.node_max) / area(b.node_min[:1], b.node_max[:1])[0]
+leaf = b.count > 0
+print(float((a[~leaf] * 1.2).sum() + (a[leaf] * b.count[leaf]).sum()))
+"""
+
+
+def test_sweep_and_binned_sah_builds_validate():
+    """The builder's two split searches (32-bin SAH, exact sweep SAH for small
+    nodes; MDRT_SAH_SWEEP sets the switch-over) both produce valid trees; on this
+    seeded 3000-triangle soup the sweep lowers the tree's SAH cost (54.13 bins
+    only, 53.87 default, 53.60 all-sweep when written)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    costs = {}
+    for sw in ("0", "1024", "100000"):
+        env = dict(os.environ, MDRT_SAH_SWEEP=sw)
+        res = subprocess.run([sys.executable, "-c", _SAH_SCRIPT, root], env=env, capture_output=True, text=True,
+                             timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        costs[sw] = float(res.stdout.strip().splitlines()[-1])
+    assert costs["100000"] <= costs["1024"] <= costs["0"], costs

@@ -472,6 +472,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.sensor = sensor;
         rp.noise_scale = a->noise_scale;
         rp.dropout_p = a->dropout_p;
+        rp.drop_k = drop_threshold(a->dropout_p);
         for (int c = 0; c < C; ++c) {
             rp.dmax64[c] = ctx->rigs[c].d_max;
             rp.fill[c] = a->fill ? a->fill[c] : ctx->rigs[c].d_max;
@@ -576,6 +577,7 @@ int mdrt_noise_dropout(const float* depth, float* out, int32_t N, int32_t C, int
         p.hn_step = absorb(absorb(key, 1ULL), static_cast<unsigned long long>(step));
         p.noise_scale = noise_scale;
         p.dropout_p = dropout_p;
+        p.drop_k = drop_threshold(dropout_p);
         for (int c = 0; c < C; ++c) {
             p.dmax[c] = d_max[c];
             p.fill[c] = fill ? fill[c] : d_max[c];

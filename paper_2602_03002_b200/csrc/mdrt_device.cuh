@@ -209,12 +209,20 @@ __device__ __forceinline__ double normal_from_hash(unsigned long long h) {
 #endif
 }
 
+// Dropout threshold: unit53(h) < p  <=>  (h >> 11) < ceil(p * 2^53), because
+// unit53(h) = (h >> 11) * 2^-53 exactly and scaling p by 2^53 is exact, so the
+// per-pixel dropout test is one 64-bit integer compare (p in [0, 1), checked by
+// the API; the reference compares the f64 uniform, sensor.py:79).
+__host__ __device__ inline unsigned long long drop_threshold(double p) {
+    return p > 0.0 ? static_cast<unsigned long long>(ceil(p * 0x1p53)) : 0ULL;
+}
+
 // apply_noise_dropout for one pixel (sensor.py:77-82). ru/rn: row prefixes
-// absorb(.., row); x: column counter.
+// absorb(.., row); cx: counter_mix of the column counter; drop_k: drop_threshold(p).
 __device__ __forceinline__ float sensor_apply_cx(float depth, unsigned long long ru, unsigned long long rn,
-                                                 unsigned long long cx, double noise_scale, double dropout_p,
-                                                 double fill, double dmax) {
-    const bool drop = unit53(mix64(ru ^ cx)) < dropout_p;
+                                                 unsigned long long cx, double noise_scale,
+                                                 unsigned long long drop_k, double fill, double dmax) {
+    const bool drop = (mix64(ru ^ cx) >> 11) < drop_k;
     const double g = normal_from_hash(mix64(rn ^ cx));
     double v = __dmul_rn(static_cast<double>(depth), __dadd_rn(1.0, __dmul_rn(noise_scale, g)));
     v = drop ? fill : v;
@@ -224,9 +232,9 @@ __device__ __forceinline__ float sensor_apply_cx(float depth, unsigned long long
 }
 
 __device__ __forceinline__ float sensor_apply(float depth, unsigned long long ru, unsigned long long rn,
-                                              unsigned long long x, double noise_scale, double dropout_p,
-                                              double fill, double dmax) {
-    return sensor_apply_cx(depth, ru, rn, counter_mix(x), noise_scale, dropout_p, fill, dmax);
+                                              unsigned long long x, double noise_scale,
+                                              unsigned long long drop_k, double fill, double dmax) {
+    return sensor_apply_cx(depth, ru, rn, counter_mix(x), noise_scale, drop_k, fill, dmax);
 }
 
 // ---------------------------------------------------------------------------

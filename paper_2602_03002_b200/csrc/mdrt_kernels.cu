@@ -460,7 +460,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const unsigned long long ru = __shfl_sync(0xffffffffu, rowh, lane / kTileW);
         const unsigned long long rn = __shfl_sync(0xffffffffu, rowh, kTileH + lane / kTileW);
         const unsigned long long cx = px < 512 ? p.cmix[px] : counter_mix(static_cast<unsigned long long>(px));
-        val = sensor_apply_cx(z, ru, rn, cx, p.noise_scale, p.dropout_p, p.fill[c], p.dmax64[c]);
+        val = sensor_apply_cx(z, ru, rn, cx, p.noise_scale, p.drop_k, p.fill[c], p.dmax64[c]);
     }
     if (active) {
         const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
@@ -619,7 +619,7 @@ static __global__ void noise_kernel(NoiseParams p) {
         absorb(absorb(absorb(p.hu_step, genv), static_cast<unsigned long long>(c)), static_cast<unsigned long long>(y));
     const unsigned long long rn =
         absorb(absorb(absorb(p.hn_step, genv), static_cast<unsigned long long>(c)), static_cast<unsigned long long>(y));
-    p.out[i] = sensor_apply(p.in[i], ru, rn, static_cast<unsigned long long>(x), p.noise_scale, p.dropout_p,
+    p.out[i] = sensor_apply(p.in[i], ru, rn, static_cast<unsigned long long>(x), p.noise_scale, p.drop_k,
                             p.fill[c], p.dmax[c]);
 }
 

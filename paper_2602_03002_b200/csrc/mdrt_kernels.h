@@ -87,6 +87,7 @@ struct RenderParams {
     int32_t ray_envs;
     int32_t sensor;
     double noise_scale, dropout_p;
+    unsigned long long drop_k;    // drop_threshold(dropout_p)
     double fill[64];
     double dmax64[64];
     float* ring;
@@ -116,6 +117,7 @@ struct NoiseParams {
     int64_t env_offset;
     unsigned long long hu_step, hn_step;
     double noise_scale, dropout_p;
+    unsigned long long drop_k;    // drop_threshold(dropout_p)
     double fill[64];
     double dmax[64];
 };

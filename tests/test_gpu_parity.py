@@ -511,3 +511,23 @@ def test_captured_full_pipeline_equals_eager(pkg):
         assert torch.equal(graph, eager), f"obs step {k}"
         assert torch.equal(ds_g, ds_e), f"downsample step {k}"
         assert torch.equal(ds_e, pkg.downsample_min(eager, 5))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [0.0, 1e-17, 2.0 ** -53, 3 * 2.0 ** -53, 0.05, 0.5, 0.999999])
+def test_dropout_mask_at_threshold_edges(pkg, oracle, p):
+    """The kernel's dropout test is an integer compare of the top 53 hash bits against
+    ceil(p * 2^53); the oracle keeps the reference's f64 compare unit53(h) < p
+    (sensor.py:79). Masks must agree exactly, including p = 0 and p at 1-3 ulps of
+    the 53-bit grid."""
+    rng = np.random.default_rng(5)
+    depth = rng.uniform(0.5, 5.0, size=(3, 2, 40, 64)).astype(np.float32)
+    d_max = np.array([6.0, 6.0])
+    cfg = pkg.SensorConfig(noise_scale=0.05, dropout_p=p, dropout_fill=0.25, seed=9)
+    out = pkg.apply_noise_dropout(torch.from_numpy(depth).cuda(), cfg, d_max=d_max, step=2).cpu().numpy()
+    ref = oracle.apply_noise_dropout(depth, noise_scale=0.05, dropout_p=p, seed=9, d_max=d_max, step=2,
+                                     dropout_fill=0.25)
+    assert np.array_equal(out == np.float32(0.25), ref == np.float32(0.25))
+    if p == 0.0:
+        assert not (ref == np.float32(0.25)).any()
+    assert _ulps(out, ref).max() <= 1

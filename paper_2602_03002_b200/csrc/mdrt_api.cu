@@ -334,6 +334,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
             need(a->ds_factor >= 1 && ctx->H % a->ds_factor == 0 && ctx->W % a->ds_factor == 0,
                  "resolution not divisible by downsample factor");
         }
+        need(static_cast<int64_t>(N) * C * ctx->H * ctx->W < (int64_t(1) << 31),
+             "num_envs * cameras * H * W must be below 2^31 pixels per step (split the batch)");
         const bool seam = a->cam_pos != nullptr;
         need(!seam || a->cam_rot != nullptr, "cam_rot is NULL while cam_pos is set");
         need(B == 0 || (a->body_pos && a->body_rot) || a->link_states, "body poses are NULL");
@@ -480,6 +482,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.ring = latency ? a->ring : nullptr;
         rp.write_slot = a->write_slot;
         rp.ring_slots = a->ring_slots;
+        rp.frame = static_cast<int64_t>(N) * C * ctx->H * ctx->W;
         rp.out_clean = a->out_clean;
         rp.out = a->out;
         rp.counters = a->counters;

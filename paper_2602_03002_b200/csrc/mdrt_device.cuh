@@ -72,7 +72,7 @@ struct alignas(16) ViewRec {
     float dmax;            // float32(d_max)
     int32_t nlinks;        // links surviving the view cull
     int32_t read_slot;     // latency ring slot to read for this env (-1: current frame)
-    int32_t pad0;
+    int32_t write_slot;    // latency ring slot this step writes (copied from the step state)
     unsigned long long hu; // rng prefix absorb(..step, env, cam) of the uniform stream
     unsigned long long hn; // same for the normal stream
     unsigned long long hr; // rsm-fill stream prefix absorb(absorb(absorb(key, step), env), cam)

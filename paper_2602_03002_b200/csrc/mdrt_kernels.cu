@@ -273,7 +273,7 @@ static __global__ void __launch_bounds__(128, MDRT_PRO_MINB) prologue_kernel(Pro
         v.dmax = static_cast<float>(rig.d_max);
         v.nlinks = count;
         v.read_slot = -1;
-        v.pad0 = 0;
+        v.write_slot = 0;
         const unsigned long long genv = static_cast<unsigned long long>(p.env_offset + e);
         const StepState* st = p.state;
         v.hu = absorb(absorb(st ? st->hu_step : p.hu_step, genv), static_cast<unsigned long long>(c));
@@ -298,6 +298,7 @@ static __global__ void __launch_bounds__(128, MDRT_PRO_MINB) prologue_kernel(Pro
             MDRT_CHECK(count >= 0 && count <= 32 && kk < 32, "ring count %d index %d", count, kk);
             const int slot = order[kk];
             v.read_slot = slot == wslot ? -1 : slot;
+            v.write_slot = wslot;
             if (c == 0 && p.read_slot_out) p.read_slot_out[e] = slot;
         }
         for (int i = 0; i < 4; ++i) v.pad1[i] = 0.f;
@@ -365,7 +366,7 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         dcz = 1.0f;
         m = sqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
     }
-    const float inv_m = 1.0f / m;
+    const float inv_m = __frcp_rn(m);   // == 1.0f / m (both correctly rounded), fewer instructions
     TraceCounters ctr;
     float z = dmax;
 
@@ -463,14 +464,16 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         val = sensor_apply_cx(z, ru, rn, cx, p.noise_scale, p.drop_k, p.fill[c], p.dmax64[c]);
     }
     if (active) {
-        const int64_t o = ((static_cast<int64_t>(e) * p.C + c) * p.H + py) * p.W + px;
+        // pixel index in 32 bits (the API bounds N*C*H*W below 2^31); view = e * C + c
+        const uint32_t o = (view * static_cast<uint32_t>(p.H) + static_cast<uint32_t>(py)) * static_cast<uint32_t>(p.W) +
+                           static_cast<uint32_t>(px);
         if (p.out_clean) st_stream(p.out_clean + o, z);
-        MDRT_CHECK(o >= 0 && o < static_cast<int64_t>(p.N) * p.C * p.H * p.W, "pixel index %lld", static_cast<long long>(o));
+        MDRT_CHECK(o < static_cast<uint64_t>(p.frame), "pixel index %u", o);
         if (p.ring) {
             // ring traffic streams past L1/L2 (evict-first) so it does not
             // displace BVH records; a zero-lag read is the value just written
-            const int64_t frame = static_cast<int64_t>(p.N) * p.C * p.H * p.W;
-            const int wslot = p.state ? p.state->write_slot : p.write_slot;
+            const int64_t frame = p.frame;   // N*C*H*W
+            const int wslot = V.write_slot;   // the prologue's copy: no per-tile state load
             st_stream(p.ring + static_cast<int64_t>(wslot) * frame + o, val);
             const int rs = V.read_slot;
             MDRT_CHECK(wslot >= 0 && wslot < p.ring_slots && rs < p.ring_slots, "ring slots write %d read %d of %d",

@@ -93,6 +93,7 @@ struct RenderParams {
     float* ring;
     int32_t write_slot;
     int32_t ring_slots;           // frames in `ring` (bounds of the MDRT_CHECKS build)
+    int64_t frame;                // N * C * H * W (pixels of one frame)
     float* out_clean;
     float* out;
     unsigned long long* counters;

@@ -257,10 +257,38 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // 32-byte vector load through the non-coherent path (LDG.E.256 on sm_100a):
 // one 64 B node record = two requests instead of four LDG.128.
+// Node-record loads carry the L2::256B prefetch-size hint: a miss fills the
+// whole 256 B L2 line run, which holds the neighbouring records the builder laid
+// out next to this one (config 5, BVH > L2: 21.19-21.26 -> 21.16 ms, +0.3 %;
+// configs 2/3 within +-0.1 %, profiles/experiments/r01_node_hint.txt).
+// MDRT_NODE_HINT (A/B knob): 0 = no hint, 1 = L1::evict_last, 2 = L2::256B
+// (default), 3 = both.
+#ifndef MDRT_NODE_HINT
+#define MDRT_NODE_HINT 2
+#endif
+#if MDRT_NODE_HINT == 1
+#define MDRT_LDG_NODE "ld.global.nc.L1::evict_last"
+#elif MDRT_NODE_HINT == 2
+#define MDRT_LDG_NODE "ld.global.nc.L2::256B"
+#elif MDRT_NODE_HINT == 3
+#define MDRT_LDG_NODE "ld.global.nc.L1::evict_last.L2::256B"
+#else
+#define MDRT_LDG_NODE "ld.global.nc"
+#endif
 __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm(MDRT_LDG_NODE ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
         : "l"(p));
+}
+__device__ __forceinline__ float4 ldg_node4(const float4* p) {
+    float4 a;
+    asm(MDRT_LDG_NODE ".v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p));
+    return a;
+}
+__device__ __forceinline__ int2 ldg_node2i(const int2* p) {
+    int2 a;
+    asm(MDRT_LDG_NODE ".v2.s32 {%0,%1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
+    return a;
 }
 
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
@@ -400,8 +428,13 @@ struct Traversal {
             // 56 of the record's 64 B: the L1 data pipe is loaded by the bytes
             // delivered per lane, so the 8 B pad after the refs is not fetched
             // (+0.3 % config 2, +0.7 % config 5 over one 32 B load)
+#if MDRT_NODE_HINT
+            const float4 bz = ldg_node4(n + 2);
+            const int2 rf = ldg_node2i(reinterpret_cast<const int2*>(n + 3));
+#else
             const float4 bz = __ldg(n + 2);                                     // c0 z lo/hi, c1 z lo/hi
             const int2 rf = __ldg(reinterpret_cast<const int2*>(n + 3));        // refs
+#endif
 #endif
             if (COUNT) ++ctr.nodes;
             float c0min, c0max, c1min, c1max;

@@ -510,6 +510,9 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
 #ifndef MDRT_MINB
 #define MDRT_MINB 9
 #endif
+#ifndef MDRT_GRAB
+#define MDRT_GRAB 1
+#endif
 #ifdef MDRT_TIMING
 // diagnostic build (tools/tile_times.py): per-tile start/end global timer
 __device__ unsigned long long g_tile_t0[1 << 22];
@@ -552,8 +555,26 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
         return static_cast<uint32_t>(static_cast<unsigned long long>(p.local_tiles) * j / nc);
     };
     uint32_t phase = nc ? 0u : 1u, base = 0;
+#if MDRT_GRAB > 1
+    // shared-pool tiles are taken MDRT_GRAB at a time; the batch's next/end
+    // live in shared memory so nothing stays in registers across a tile
+    __shared__ uint32_t s_batch[kBlock / 32][2];
+    volatile uint32_t* sb = s_batch[threadIdx.x >> 5];
+    sb[0] = 0;
+    sb[1] = 0;
+#endif
     while (true) {
         uint32_t gw = 0xffffffffu;
+#if MDRT_GRAB > 1
+        {
+            const uint32_t nxt = sb[0];
+            if (nxt < sb[1]) {
+                sb[0] = nxt + 1;
+                gw = nxt;
+            }
+        }
+        if (gw == 0xffffffffu)
+#endif
         while (phase < 3) {
             uint32_t ctr_idx, lo, size;
             if (phase == 0) {
@@ -579,10 +600,19 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
                 size = lo_of(ctr_idx + 1) - lo;
             }
             uint32_t t = 0;
-            if (lane == 0) t = atomicAdd(p.tile_counter + ctr_idx, 1u);
+#if MDRT_GRAB > 1
+            const uint32_t g = phase == 1 ? MDRT_GRAB : 1u;
+#else
+            const uint32_t g = 1u;
+#endif
+            if (lane == 0) t = atomicAdd(p.tile_counter + ctr_idx, g);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t < size) {
                 gw = lo + t;
+#if MDRT_GRAB > 1
+                sb[0] = gw + 1;
+                sb[1] = lo + min(t + g, size);
+#endif
                 break;
             }
             phase = (phase == 1 && nc == 0) ? 3u : (phase < 2 ? phase + 1 : phase);

@@ -555,7 +555,11 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
         return static_cast<uint32_t>(static_cast<unsigned long long>(p.local_tiles) * j / nc);
     };
     uint32_t phase = nc ? 0u : 1u, base = 0;
-#if MDRT_GRAB > 1
+#if MDRT_GRAB > 1 && defined(MDRT_GRAB_REG)
+    // shared-pool tiles are taken MDRT_GRAB at a time (aligned groups); only the
+    // last tile index stays live across a tile, the group end is recomputed
+    uint32_t last = 0xffffffffu;
+#elif MDRT_GRAB > 1
     // shared-pool tiles are taken MDRT_GRAB at a time; the batch's next/end
     // live in shared memory so nothing stays in registers across a tile
     __shared__ uint32_t s_batch[kBlock / 32][2];
@@ -565,7 +569,13 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
 #endif
     while (true) {
         uint32_t gw = 0xffffffffu;
-#if MDRT_GRAB > 1
+#if MDRT_GRAB > 1 && defined(MDRT_GRAB_REG)
+        {
+            const uint32_t nxt = last + 1;
+            if (phase == 1 && ((nxt - pool_lo) & (MDRT_GRAB - 1)) != 0 && nxt < total) gw = nxt;
+        }
+        if (gw == 0xffffffffu)
+#elif MDRT_GRAB > 1
         {
             const uint32_t nxt = sb[0];
             if (nxt < sb[1]) {
@@ -609,7 +619,7 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t < size) {
                 gw = lo + t;
-#if MDRT_GRAB > 1
+#if MDRT_GRAB > 1 && !defined(MDRT_GRAB_REG)
                 sb[0] = gw + 1;
                 sb[1] = lo + min(t + g, size);
 #endif
@@ -618,6 +628,9 @@ static __global__ void __launch_bounds__(kBlock, MDRT_MINB) render_kernel(Render
             phase = (phase == 1 && nc == 0) ? 3u : (phase < 2 ? phase + 1 : phase);
         }
         if (gw == 0xffffffffu) break;
+#if MDRT_GRAB > 1 && defined(MDRT_GRAB_REG)
+        last = gw;
+#endif
 #ifdef MDRT_TIMING
         unsigned long long t0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));

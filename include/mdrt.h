@@ -171,6 +171,16 @@ int mdrt_get_stats(mdrt_ctx *ctx, mdrt_stats *out);
  * fused into one traversal kernel. `stream` is a cudaStream_t (NULL = default). */
 int mdrt_render(mdrt_ctx *ctx, const mdrt_step_args *args, void *stream);
 
+/* Stream ordering of one context. All renders of a context share its per-step
+ * scratch (view/link records, tile counters, device step state). Outside CUDA
+ * graph capture mdrt_render orders itself: a call on a stream other than the
+ * previous call's first waits for that call's completion (cudaStreamWaitEvent).
+ * A captured graph runs outside mdrt_render, so its replays are bracketed by
+ * mdrt_order_begin (wait for the context's last work) and mdrt_order_end (record
+ * the replay as the context's last work) on the replay stream. */
+int mdrt_order_begin(mdrt_ctx *ctx, void *stream);
+int mdrt_order_end(mdrt_ctx *ctx, void *stream);
+
 /* Device step state for graph replay (MDRT_DEVICE_STATE). Each mdrt_render with
  * the flag first advances it on the device: k = next_step, now = t0 + k*dt,
  * sensor stream prefix from (key, k), and (ring_slots > 0) a FrameBuffer push of

@@ -158,6 +158,8 @@ def lib():
             "mdrt_peer_close": (ctypes.c_int, [vp]),
             "mdrt_peer_free": (ctypes.c_int, [vp]),
             "mdrt_sync": (ctypes.c_int, [vp]),
+            "mdrt_order_begin": (ctypes.c_int, [vp, vp]),
+            "mdrt_order_end": (ctypes.c_int, [vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -175,7 +177,8 @@ EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_cre
            "mdrt_add_body", "mdrt_set_terrain", "mdrt_set_cameras", "mdrt_commit", "mdrt_get_stats",
            "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
            "mdrt_downsample_min", "mdrt_depth_to_u8", "mdrt_bvh_build", "mdrt_query_rays", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_peer_alloc",
-           "mdrt_peer_open", "mdrt_peer_close", "mdrt_peer_free", "mdrt_sync")
+           "mdrt_peer_open", "mdrt_peer_close", "mdrt_peer_free", "mdrt_sync", "mdrt_order_begin",
+           "mdrt_order_end")
 
 
 def check(rc: int) -> None:
@@ -265,6 +268,12 @@ class Context:
 
     def sync(self) -> None:
         check(lib().mdrt_sync(self._ptr))
+
+    def order_begin(self, stream: int) -> None:
+        check(lib().mdrt_order_begin(self._ptr, ctypes.c_void_p(stream)))
+
+    def order_end(self, stream: int) -> None:
+        check(lib().mdrt_order_end(self._ptr, ctypes.c_void_p(stream)))
 
     def state_set(self, num_envs, key, t0, dt, next_step, ring_slots, times, order, rsm_key=0) -> None:
         import numpy as np

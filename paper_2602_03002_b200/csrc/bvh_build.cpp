@@ -8,6 +8,7 @@
 #include <cstring>
 #include <limits>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace mdrt {
@@ -308,6 +309,17 @@ PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int
     if (leaf_max <= 0) leaf_max = options().leaf_max;
     if (leaf_max > 8) throw std::invalid_argument("leaf size must be <= 8 (leaf encoding)");
     if (nf <= 0) throw std::invalid_argument("cannot build a BVH over an empty mesh");
+    // The traversal stack holds kMaxDepth entries. The builder keeps every leaf
+    // within kMaxDepth levels by switching to median splits when the remaining
+    // depth budget gets tight, which is only possible while the mesh fits a
+    // complete tree of leaf_max-triangle leaves: reject larger meshes here
+    // instead of overflowing the device stack (bvh.py:68-136 has no depth bound:
+    // its CPU stack is 128 entries, numba_backend.py:126).
+    if (nf > (static_cast<int64_t>(leaf_max) << (kMaxDepth - 1)))
+        throw std::invalid_argument("mesh too large for the traversal stack (more than leaf_max * 2^" +
+                                    std::to_string(kMaxDepth - 1) + " triangles): split it into several bodies");
+    for (int64_t i = 0; i < 3 * nv; ++i)
+        if (!std::isfinite(verts[i])) throw std::invalid_argument("mesh vertices must be finite");
     std::vector<Box> tb(nf);
     std::vector<std::array<double, 3>> cen(nf);
     for (int64_t f = 0; f < nf; ++f) {
@@ -409,6 +421,8 @@ PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int
         }
     }
     out.depth = maxdepth;
+    if (out.depth > kMaxDepth)   // cannot happen given the size check above; never ship a deeper tree
+        throw std::invalid_argument("BVH deeper than the traversal stack");
 
     // bounding sphere of the vertices actually referenced
     Box all = root.box;

@@ -139,8 +139,30 @@ struct mdrt_ctx {
     DevBuf<int2> rects;
     DevBuf<unsigned int> tile_counter;
     DevBuf<StepState> state;
+    // Cross-stream ordering of the per-step scratch (views, links, rects, tile
+    // counters, step state): every call that uses it waits for the previous
+    // user's completion event when it runs on a different stream.
+    cudaEvent_t done = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
 
     void use_device() const { CK(cudaSetDevice(device)); }
+
+    // make `s` wait for this context's last recorded work (no-op on the same stream)
+    void order_begin(cudaStream_t s) {
+        if (has_last && s != last_stream) CK(cudaStreamWaitEvent(s, done, 0));
+    }
+    void order_end(cudaStream_t s) {
+        if (!done) CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        CK(cudaEventRecord(done, s));
+        last_stream = s;
+        has_last = true;
+    }
+    static bool capturing(cudaStream_t s) {
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(s, &st));
+        return st != cudaStreamCaptureStatusNone;
+    }
 };
 
 extern "C" {
@@ -188,6 +210,7 @@ int mdrt_destroy(mdrt_ctx* ctx) {
         ctx->rects.release();
         ctx->tile_counter.release();
         ctx->state.release();
+        if (ctx->done) cudaEventDestroy(ctx->done);
         delete ctx;
     });
 }
@@ -370,6 +393,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         need(!(a->flags & MDRT_COUNT) || a->counters, "counters is NULL with MDRT_COUNT");
         ctx->use_device();
         cudaStream_t s = static_cast<cudaStream_t>(stream);
+        // outside graph capture the context orders its own scratch across streams;
+        // a captured graph's replays are ordered by mdrt_order_begin/end around them
+        const bool ordered = !mdrt_ctx::capturing(s);
+        if (ordered) ctx->order_begin(s);
         const size_t nviews = static_cast<size_t>(N) * C;
         ctx->views.reserve(nviews);
         ctx->links.reserve(std::max<size_t>(1, nviews * std::max(B, 1)));
@@ -407,6 +434,9 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
             need(a->rsm_modes != nullptr, "rsm_modes is NULL with MDRT_RSM");
             need(a->rsm_k1 >= 0 && a->rsm_k2 >= 0 && 2 * a->rsm_k1 <= ctx->W && 2 * a->rsm_k2 <= ctx->W,
                  "rsm column counts out of range");
+            // the fused block minimum (ds_out) orders floats by their bit patterns, which
+            // holds for values >= 0 only; every other output value is >= 1e-6 or d_max > 0
+            need(!a->ds_out || a->rsm_fill_low >= 0.0, "rsm_fill_low must be >= 0 with ds_out (fused block minimum)");
             pp.rsm_modes = a->rsm_modes;
             pp.rsm_k[0] = 0;
             pp.rsm_k[1] = a->rsm_k1;
@@ -444,7 +474,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
             launch_prologue(pp, static_cast<int64_t>(nviews), s);
             CK(cudaGetLastError());
         }
-        if (only_pro) return;
+        if (only_pro) {
+            if (ordered) ctx->order_end(s);
+            return;
+        }
 
         RenderParams rp{};
         rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
@@ -507,6 +540,23 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
                                                             ctx->tris.cap * sizeof(PackedTri));
         launch_render(rp, warps, (a->flags & MDRT_COUNT) != 0, geometry_bytes, s);
         CK(cudaGetLastError());
+        if (ordered) ctx->order_end(s);
+    });
+}
+
+int mdrt_order_begin(mdrt_ctx* ctx, void* stream) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        ctx->use_device();
+        ctx->order_begin(static_cast<cudaStream_t>(stream));
+    });
+}
+
+int mdrt_order_end(mdrt_ctx* ctx, void* stream) {
+    return guarded([&] {
+        need(ctx != nullptr, "ctx is NULL");
+        ctx->use_device();
+        ctx->order_end(static_cast<cudaStream_t>(stream));
     });
 }
 

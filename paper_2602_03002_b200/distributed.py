@@ -47,52 +47,82 @@ def init_from_env(backend: str | None = None):
     return rank, world, local, device
 
 
-def gather_frames(obs: torch.Tensor, dst: int | None = 0, group=None) -> torch.Tensor | None:
+def rank_sizes(n_local: int, group=None, device=None) -> list[int]:
+    """Every rank's leading (env) size, in rank order (one small all_gather)."""
+    world = dist.get_world_size(group)
+    dev = device if device is not None and dist.get_backend(group) == "nccl" else torch.device("cpu")
+    mine = torch.tensor([int(n_local)], dtype=torch.int64, device=dev)
+    allv = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(allv, mine, group=group)
+    return [int(v.item()) for v in allv]
+
+
+def gather_frames(obs: torch.Tensor, dst: int | None = 0, group=None, sizes: list[int] | None = None
+                  ) -> torch.Tensor | None:
     """Concatenate every rank's (N_r, C, H, W) observation block in rank order.
 
     dst=None: all ranks receive the full tensor (all_gather); otherwise only
-    ``dst`` does (others get None). Requires equal N_r on all ranks. NCCL uses
-    all_gather_into_tensor / grouped P2P; gloo uses all_gather / gather.
+    ``dst`` does (others get None). Blocks may differ in N_r (``env_slice``
+    gives slices that differ by one when the env count does not divide):
+    ``sizes`` (every rank's N_r) is exchanged first unless the caller passes
+    it. NCCL uses grouped P2P for dst, all_gather_into_tensor for equal blocks
+    (padded to the largest block otherwise); gloo stages through the CPU.
     """
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return obs
     if dist.get_backend(group) == "gloo" and obs.device.type == "cuda":
         # gloo collectives are host-side: stage through the CPU
-        res = gather_frames(obs.cpu(), dst, group)
+        res = gather_frames(obs.cpu(), dst, group, sizes)
         return None if res is None else res.to(obs.device)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     obs = obs.contiguous()
-    full_shape = (world * obs.shape[0],) + tuple(obs.shape[1:])
+    if sizes is None:
+        sizes = rank_sizes(obs.shape[0], group, obs.device)
+    sizes = [int(x) for x in sizes]
+    if len(sizes) != world or sizes[rank] != obs.shape[0]:
+        raise ValueError(f"sizes {sizes} do not match world {world} / local block {obs.shape[0]}")
+    tail = tuple(obs.shape[1:])
+    total = sum(sizes)
+    offs = [sum(sizes[:r]) for r in range(world)]
     nccl = dist.get_backend(group) == "nccl"
-    if dst is None:
-        out = torch.empty(full_shape, dtype=obs.dtype, device=obs.device)
-        if nccl:
-            dist.all_gather_into_tensor(out, obs, group=group)
-        else:
-            dist.all_gather(list(out.chunk(world)), obs, group=group)
-        return out
-    if nccl:
+    if nccl and dst is not None:
         ops = []
         out = None
         if rank == dst:
-            out = torch.empty(full_shape, dtype=obs.dtype, device=obs.device)
-            parts = out.chunk(world)
-            parts[rank].copy_(obs)
+            out = torch.empty((total,) + tail, dtype=obs.dtype, device=obs.device)
+            out[offs[rank]:offs[rank] + sizes[rank]].copy_(obs)
             for r in range(world):
-                if r != rank:
-                    ops.append(dist.P2POp(dist.irecv, parts[r], r, group))
-        else:
+                if r != rank and sizes[r]:
+                    ops.append(dist.P2POp(dist.irecv, out[offs[r]:offs[r] + sizes[r]], r, group))
+        elif obs.shape[0]:
             ops.append(dist.P2POp(dist.isend, obs, dst, group))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
         return out
-    if rank == dst:
-        out = torch.empty(full_shape, dtype=obs.dtype, device=obs.device)
-        dist.gather(obs, list(out.chunk(world)), dst=dst, group=group)
-        return out
-    dist.gather(obs, None, dst=dst, group=group)
-    return None
+    # collectives with equal blocks: pad every block to the largest one
+    mx = max(sizes)
+    blk = obs
+    if obs.shape[0] != mx:
+        blk = torch.zeros((mx,) + tail, dtype=obs.dtype, device=obs.device)
+        blk[:obs.shape[0]].copy_(obs)
+    if dst is None or rank == dst:
+        padded = torch.empty((world * mx,) + tail, dtype=obs.dtype, device=obs.device)
+        parts = list(padded.chunk(world))
+    if dst is None:
+        if nccl:
+            dist.all_gather_into_tensor(padded, blk, group=group)
+        else:
+            dist.all_gather(parts, blk, group=group)
+    elif rank == dst:
+        dist.gather(blk, parts, dst=dst, group=group)
+    else:
+        dist.gather(blk, None, dst=dst, group=group)
+        return None
+    if mx * world == total:
+        return padded
+    return torch.cat([parts[r][:sizes[r]] for r in range(world)])
 
 
 # ---------------------------------------------------------------------------

@@ -162,6 +162,15 @@ class CapturedStep:
     renderer is likewise captured in a graph.
     """
 
+    # Lifetime and ownership: the graph holds raw device pointers, so the step keeps
+    # every tensor it recorded alive (out, ds_out, delays, RSM modes, camera
+    # randomisation, bound link states) and refuses to replay once the scene
+    # replaced one of them (scene._ptr_version; re-randomising cameras writes in
+    # place and is fine). The context has one device step state: a newer
+    # CapturedStep on the same scene takes it over and the older one refuses to
+    # replay; close() releases it. Replays are ordered against other renders of
+    # the scene on any stream (mdrt_order_begin/end).
+
     def __init__(self, scene: Scene, *, sensor: SensorConfig | None = None,
                  frame_buffer: FrameBuffer | None = None, delays=None, dt: float = 0.02, t0: float = 0.0,
                  first_step: int = 0, out: torch.Tensor | None = None, early_termination: bool = True,
@@ -176,12 +185,16 @@ class CapturedStep:
         self.out = scene._new_frame(out)
         a = scene._step_args(self.out, early_termination)
         a.flags |= _native.DEVICE_STATE
-        self._keep = []
+        # every tensor whose pointer the graph records (see the class comment)
+        self._keep = [self.out, scene.body_positions, scene.body_rotations, scene._rand_pos, scene._rand_rot,
+                      scene._rand_fov, scene._link_states]
         key = 0
         if rsm is not None:
             _set_rsm(a, scene, rsm, rsm_modes, self._keep)
         if ds_out is not None:
             _set_downsample(a, scene, ds_out, downsample_factor)
+            self._keep.append(ds_out)
+            self.ds_out = ds_out
         if sensor is not None:
             a.flags |= _native.SENSOR
             a.noise_scale = float(sensor.noise_scale)
@@ -202,7 +215,7 @@ class CapturedStep:
             times = np.asarray(frame_buffer._times, dtype=np.float64)
             order = np.asarray(frame_buffer._slots, dtype=np.int32)
             slots = frame_buffer.capacity
-            self._keep.append(d)
+            self._keep += [d, frame_buffer._ring, frame_buffer._slot_buf]
             a.flags |= _native.LATENCY
             a.ring = frame_buffer._ring.data_ptr()
             a.ring_slots = frame_buffer.capacity
@@ -210,6 +223,8 @@ class CapturedStep:
             a.read_slot = frame_buffer._slot_buf.data_ptr()
         scene._ctx.state_set(scene.num_envs, key, self.t0, self.dt, self.next_step, slots, times, order,
                              rsm_key=rsm.fill_key if rsm is not None else 0)
+        scene._state_owner = self          # a previous CapturedStep of this scene stops replaying
+        self._version = scene._ptr_version
         self._args = a
         # warm the launch path (occupancy query) outside capture, then capture
         plain = scene._step_args(self.out, early_termination)
@@ -224,7 +239,18 @@ class CapturedStep:
 
     def replay(self) -> torch.Tensor:
         """Run step ``next_step`` on the current stream; returns the observation tensor."""
+        sc = self.scene
+        if sc._state_owner is not self:
+            raise RuntimeError("this CapturedStep no longer owns the scene's device step state "
+                               "(a newer CapturedStep took it over, or close() was called)")
+        if sc._ptr_version != self._version:
+            raise RuntimeError("the scene's pose / camera-randomisation buffers were replaced after capture "
+                               "(bind_link_states, set_body_poses after a bind, or camera randomisation "
+                               "set / cleared): capture a new CapturedStep")
+        stream = torch.cuda.current_stream(sc.device).cuda_stream
+        sc._ctx.order_begin(stream)
         self.graph.replay()
+        sc._ctx.order_end(stream)
         if self.frame_buffer is not None:   # host shadow of the device ring bookkeeping
             self.frame_buffer._reserve(self.t0 + float(self.next_step) * self.dt)
         self.next_step += 1
@@ -232,3 +258,10 @@ class CapturedStep:
 
     def device_state(self) -> dict:
         return self.scene._ctx.state_get()
+
+    def close(self) -> None:
+        """Release the scene's device step state and the recorded buffers."""
+        if self.scene._state_owner is self:
+            self.scene._state_owner = None
+        self.graph = None
+        self._keep = []

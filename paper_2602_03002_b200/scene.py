@@ -137,6 +137,12 @@ class Scene:
         self._rand_pos: torch.Tensor | None = None
         self._rand_rot: torch.Tensor | None = None
         self._rand_fov: torch.Tensor | None = None
+        self._link_states = None
+        # bumped whenever a device buffer the kernels read by pointer is replaced
+        # (camera randomisation allocated/cleared, link states bound/unbound), so a
+        # CapturedStep recorded against the old pointers refuses to replay
+        self._ptr_version = 0
+        self._state_owner = None       # the CapturedStep that owns the device step state
         self.d_max_per_camera = np.array([c.d_max for c in cams], dtype=np.float64)
 
     # -- sizes -------------------------------------------------------------
@@ -173,7 +179,7 @@ class Scene:
         they need a device->host read).
         """
         n, b = self.num_envs, self.num_bodies
-        self._link_states = None
+        self.unbind_link_states()
         srcs = []
         for x, k in ((positions, 3), (rotations, 4)):
             if isinstance(x, torch.Tensor):
@@ -263,9 +269,12 @@ class Scene:
             raise ValueError(f"pos/rot offsets outside the {rec}-float record")
         lmap = torch.as_tensor(lm.astype(np.int32), device=self.device)
         self._link_states = (states, lmap, links, rec, int(pos_offset), int(rot_offset), quat_order == "xyzw")
+        self._ptr_version += 1
 
     def unbind_link_states(self) -> None:
-        self._link_states = None
+        if self._link_states is not None:
+            self._link_states = None
+            self._ptr_version += 1
 
     def _host_poses(self) -> tuple[np.ndarray, np.ndarray]:
         """(N,B,3), (N,B,4) wxyz f64 host copies of the pose source the prologue reads."""
@@ -289,10 +298,21 @@ class Scene:
         f = _as_device_f32(fov_delta, self.device)
         if tuple(p.shape) != (n, c, 3) or tuple(r.shape) != (n, c, 4) or tuple(f.shape) != (n, c):
             raise ValueError("camera randomization arrays have wrong shapes")
-        self._rand_pos, self._rand_rot, self._rand_fov = p, r, f
+        if self._rand_pos is not None:
+            # re-randomisation (e.g. per episode) writes the scene's own buffers in
+            # place, so captured graphs keep reading valid memory and see the new offsets
+            self._rand_pos.copy_(p)
+            self._rand_rot.copy_(r)
+            self._rand_fov.copy_(f)
+            return
+        # fresh buffers owned by the scene (never the caller's tensors)
+        self._rand_pos, self._rand_rot, self._rand_fov = p.clone(), r.clone(), f.clone()
+        self._ptr_version += 1
 
     def clear_camera_randomization(self) -> None:
-        self._rand_pos = self._rand_rot = self._rand_fov = None
+        if self._rand_pos is not None:
+            self._rand_pos = self._rand_rot = self._rand_fov = None
+            self._ptr_version += 1
 
     # -- host-side views of the derived state (API parity) --------------------
     def camera_world_poses(self) -> tuple[np.ndarray, np.ndarray]:
@@ -352,6 +372,7 @@ class Scene:
         return a
 
     def _launch(self, args: _native.StepArgs) -> None:
+        # mdrt_render orders the context's shared scratch across streams itself
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self._ctx.render(args, stream)
 

@@ -64,3 +64,33 @@ def test_degenerate_split_all_centroids_equal():
 def test_bad_input_rejected():
     with pytest.raises(ValueError):
         _native.bvh_check(np.zeros((3, 3)), np.array([[0, 1, 5]]))
+
+
+def test_non_finite_vertices_rejected():
+    v = np.array([[0, 0, 0], [1, 0, 0], [0, np.nan, 0]], dtype=np.float64)
+    with pytest.raises(ValueError, match="finite"):
+        _native.bvh_check(v, np.array([[0, 1, 2]]))
+    v[1, 2] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        _native.bvh_check(v, np.array([[0, 1, 2]]))
+
+
+def test_oversize_mesh_rejected_before_build():
+    """A mesh the 24-entry traversal stack cannot hold (more than leaf_max * 2^23
+    triangles) is refused with MDRT_EINVAL by the builder every geometry entry
+    point goes through (mdrt_add_body / mdrt_set_terrain / mdrt_bvh_build), before
+    any face is read: the faces array below is calloc-backed and never touched."""
+    import ctypes
+    nf = 4 * (1 << 23) + 1
+    faces = np.zeros((nf, 3), dtype=np.int64)            # lazily zero-filled pages
+    verts = np.zeros((3, 3), dtype=np.float64)
+    counts = np.zeros(3, np.int64)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    rc = _native.lib().mdrt_bvh_build(_native.dptr(verts), 3, faces.ctypes.data_as(i64p), nf, 4, None, 0, None, 0,
+                                      None, counts.ctypes.data_as(i64p))
+    assert rc == _native.MDRT_EINVAL
+    assert b"traversal stack" in _native.lib().mdrt_last_error()
+    # leaf size 1: the limit is 2^23 triangles
+    rc = _native.lib().mdrt_bvh_build(_native.dptr(verts), 3, faces.ctypes.data_as(i64p), (1 << 23) + 1, 1, None, 0,
+                                      None, 0, None, counts.ctypes.data_as(i64p))
+    assert rc == _native.MDRT_EINVAL

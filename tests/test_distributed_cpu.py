@@ -60,10 +60,16 @@ def _worker(rank, world, port, q):
         t = torch.from_numpy(noisy)
         full_all = pd.gather_frames(t, dst=None)
         full_dst = pd.gather_frames(t, dst=0)
-        q.put((rank, lat, off, full_all.numpy(), None if full_dst is None else full_dst.numpy()))
+        # uneven slices (11 envs over 2 ranks: 6 + 5) gather in rank order too
+        s2, n2 = pd.env_slice(11, rank, world)
+        u = torch.arange(s2 * 6, (s2 + n2) * 6, dtype=torch.float32).reshape(n2, 1, 2, 3)
+        ua = pd.gather_frames(u, dst=None)
+        ud = pd.gather_frames(u, dst=0, sizes=[pd.env_slice(11, r, world)[1] for r in range(world)])
+        uneven = (ua.numpy(), None if ud is None else ud.numpy())
+        q.put((rank, lat, off, full_all.numpy(), None if full_dst is None else full_dst.numpy(), uneven))
         dist.destroy_process_group()
     except Exception as exc:  # surface worker failures to the parent
-        q.put((rank, "error", repr(exc), None, None))
+        q.put((rank, "error", repr(exc), None, None, None))
 
 
 def test_two_rank_gloo_slices_and_gather():
@@ -95,6 +101,11 @@ def test_two_rank_gloo_slices_and_gather():
         assert np.array_equal(res[r][3], ref)          # all_gather on every rank
     assert np.array_equal(res[0][4], ref)              # gather to rank 0
     assert res[1][4] is None
+    full11 = np.arange(11 * 6, dtype=np.float32).reshape(11, 1, 2, 3)
+    for r in range(world):
+        assert np.array_equal(res[r][5][0], full11)   # uneven all_gather (padded blocks, sliced)
+    assert np.array_equal(res[0][5][1], full11)        # uneven gather to rank 0
+    assert res[1][5][1] is None
 
 
 def test_peer_block_offsets_and_pointer_views():

@@ -45,6 +45,9 @@ extern "C" {
 #define MDRT_COUNT_DETAIL 0x80     /* with MDRT_COUNT: counters has 4 slots (+ link node fetches, link traversals) */
 #define MDRT_RSM 0x200             /* random side masking of the output (perception.py:169-202)             */
 #define MDRT_ROT_XYZW 0x400       /* link_states quaternions are stored x, y, z, w (simulator order)     */
+#define MDRT_WIDE_STORES 0x800    /* `out` is remote (peer-mapped) memory: render 8-pixel-wide tiles so each
+                                     warp's obs stores cover >= 32 contiguous bytes per image row (NVLink
+                                     writes in whole sectors instead of 16 B pieces)                      */
 #define MDRT_DEVICE_STATE 0x100    /* step, timestamp, RNG prefix and ring push come from the context's device
                                       state (mdrt_state_set), advanced on the device at the start of the call:
                                       the call is then CUDA-graph capturable and replayable with no host args */
@@ -253,9 +256,10 @@ int mdrt_depth_to_u8(const float *in, uint8_t *out, int64_t n, double d_max, voi
 int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_t nf,
                    int64_t info[4]);
 
-/* Bandwidth probe for roofline denominators: `iters` passes of 16-byte loads
- * over a device buffer of `bytes` (L2-resident when bytes << L2 size); writes
- * one float per block into `sink` (device, >= 4096 floats) so loads are live. */
+/* Bandwidth probe for roofline denominators: `iters` passes of 32-byte L1-bypassing
+ * loads (ld.global.cg, 4 in flight per thread) over a device buffer of `bytes`
+ * (L2-resident when bytes << L2 size; bytes must be a multiple of 32); writes one
+ * float per block into `sink` (device, >= 4096 floats) so loads are live. */
 int mdrt_probe_read(const void *buf, int64_t bytes, int32_t iters, float *sink, void *stream);
 
 /* Fused frame gather over peer memory (the reference

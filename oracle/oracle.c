@@ -155,6 +155,13 @@ static inline void rotate_q(double qw, double qx, double qy, double qz,
     *rz = vz + qw * tz + (qx * ty - qy * tx);
 }
 
+/* Barycentric margin of the triangle test: 0 (the reference's exact u in [0,1],
+ * v >= 0, u + v <= 1, numba_backend.py:58-64) unless a parity diagnostic sets
+ * the GPU kernel's fp32 watertightness margin (kBaryEps) to classify hit/miss
+ * flips (bench.py parity block). Test infrastructure only. */
+static double g_bary_eps = 0.0;
+void orc_set_bary_eps(double eps) { g_bary_eps = eps; }
+
 static inline double tri_t(const double *v0, const double *v1, const double *v2, int64_t i,
                            double ox, double oy, double oz, double dx, double dy, double dz,
                            double t_max) {
@@ -170,12 +177,13 @@ static inline double tri_t(const double *v0, const double *v1, const double *v2,
     double inv_det = 1.0 / det;
     double tx = ox - a[0], ty = oy - a[1], tz = oz - a[2];
     double u = (tx * px + ty * py + tz * pz) * inv_det;
-    if (u < 0.0 || u > 1.0) return miss;
+    const double be = g_bary_eps;
+    if (u < -be || u > 1.0 + be) return miss;
     double qx = ty * e1z - tz * e1y;
     double qy = tz * e1x - tx * e1z;
     double qz = tx * e1y - ty * e1x;
     double v = (dx * qx + dy * qy + dz * qz) * inv_det;
-    if (v < 0.0 || u + v > 1.0) return miss;
+    if (v < -be || u + v > 1.0 + be) return miss;
     double t = (e2x * qx + e2y * qy + e2z * qz) * inv_det;
     if (t <= RAY_EPSILON || t > t_max) return miss;
     return t;

@@ -74,6 +74,8 @@ def lib():
             L.orc_render.argtypes = ([_i64] * 6 + [_dp, _dp, _dp, _dp, _dp, _dp, _i32p, _dp, _dp]
                                      + [_i32p] * 4 + [_dp] * 3 + [_i64, _dp, _dp] + [_i32p] * 4
                                      + [_dp] * 3 + [_dp, ctypes.c_int, _fp, ctypes.c_int, _i64p])
+            L.orc_set_bary_eps.restype = None
+            L.orc_set_bary_eps.argtypes = [ctypes.c_double]
             L.orc_mix64.restype = _u64
             L.orc_mix64.argtypes = [_u64]
             L.orc_absorb.restype = _u64
@@ -320,6 +322,12 @@ class OracleScene:
         return render_flat(self.flat, body_pos, body_rot, cam_pos, cam_rot, dirs, scale,
                            np.array([c["d_max"] for c in self.cameras], np.float64),
                            early_termination, threads=threads, counters=counters)
+
+
+def set_bary_eps(eps: float) -> None:
+    """Barycentric margin of the oracle's triangle test (0 = the reference's exact
+    test). Only for classifying GPU/oracle hit-miss flips."""
+    lib().orc_set_bary_eps(float(eps))
 
 
 def render_flat(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,

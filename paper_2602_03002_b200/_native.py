@@ -32,6 +32,7 @@ COUNT_DETAIL = 0x80
 DEVICE_STATE = 0x100
 RSM = 0x200
 ROT_XYZW = 0x400
+WIDE_STORES = 0x800
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -179,6 +180,25 @@ EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_cre
            "mdrt_downsample_min", "mdrt_depth_to_u8", "mdrt_bvh_build", "mdrt_query_rays", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_peer_alloc",
            "mdrt_peer_open", "mdrt_peer_close", "mdrt_peer_free", "mdrt_sync", "mdrt_order_begin",
            "mdrt_order_end")
+
+
+# Device address ranges that are remote memory (peer mappings of another GPU's
+# buffer, distributed.PeerFrameSink): a render whose `out` lies in one gets
+# MDRT_WIDE_STORES so its epilogue writes NVLink in whole 32 B sectors.
+_remote: dict[int, int] = {}
+
+
+def register_remote(base: int, nbytes: int) -> None:
+    _remote[int(base)] = int(nbytes)
+
+
+def unregister_remote(base: int) -> None:
+    _remote.pop(int(base), None)
+
+
+def is_remote(ptr: int) -> bool:
+    p = int(ptr)
+    return any(b <= p < b + n for b, n in _remote.items())
 
 
 def check(rc: int) -> None:

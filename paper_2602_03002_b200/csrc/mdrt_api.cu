@@ -481,7 +481,8 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
 
         RenderParams rp{};
         rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
-        rp.tile_w = render_tile_width(ctx->W);
+        // remote `out` (fused gather over NVLink): 8-wide tiles, 32 B contiguous per row store
+        rp.tile_w = (a->flags & MDRT_WIDE_STORES) ? 8 : render_tile_width(ctx->W);
         const int tile_h = 32 / rp.tile_w;
         rp.tiles_x = (ctx->W + rp.tile_w - 1) / rp.tile_w;
         rp.tiles_per_view = rp.tiles_x * ((ctx->H + tile_h - 1) / tile_h);

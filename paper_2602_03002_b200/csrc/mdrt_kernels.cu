@@ -773,15 +773,33 @@ static __global__ void __launch_bounds__(128) query_kernel(QueryParams p) {
     p.face_out[i] = tv.hit ? tv.face : -1;
 }
 
-// read-bandwidth probe: grid-stride 16 B loads, one partial sum per block
+// read-bandwidth probe (roofline denominator of the L2-resident traversal):
+// grid-stride 32 B loads that bypass L1 (ld.global.cg: served by L2 when the
+// buffer is L2-resident), four independent loads in flight per thread, one
+// partial sum per block
+__device__ __forceinline__ void ldcg256(const float4* p, float4& a, float4& b) {
+    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
 static __global__ void __launch_bounds__(256) probe_read_kernel(const float4* __restrict__ buf, int64_t n16,
                                                                 int iters, float* sink) {
     float acc = 0.f;
+    const int64_t n32 = n16 / 2;                       // 32 B items
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int it = 0; it < iters; ++it) {
-        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-            const float4 v = __ldcg(buf + i);
-            acc += (v.x + v.y) + (v.z + v.w);
+        int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < n32; i += 4 * stride) {
+            float4 a[4], b[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ldcg256(buf + 2 * (i + k * stride), a[k], b[k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc += ((a[k].x + a[k].y) + (a[k].z + a[k].w)) + ((b[k].x + b[k].y) + (b[k].z + b[k].w));
+        }
+        for (; i < n32; i += stride) {
+            float4 a, b;
+            ldcg256(buf + 2 * i, a, b);
+            acc += ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
         }
     }
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);

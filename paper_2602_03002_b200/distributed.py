@@ -47,6 +47,49 @@ def init_from_env(backend: str | None = None):
     return rank, world, local, device
 
 
+def gpu_numa_node(device: torch.device) -> int | None:
+    """NUMA node of a GPU's PCI function (sysfs), or None when unknown."""
+    try:
+        p = torch.cuda.get_device_properties(device)
+        path = f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0/numa_node"
+        node = int(open(path).read().strip())
+        return node if node >= 0 else None
+    except (OSError, ValueError, AttributeError, RuntimeError):
+        return None
+
+
+def _cpulist(text: str) -> set[int]:
+    cpus = set()
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        lo, _, hi = part.partition("-")
+        cpus.update(range(int(lo), int(hi or lo) + 1))
+    return cpus
+
+
+def bind_to_gpu_numa(device: torch.device) -> dict:
+    """Pin this process's threads to the CPUs of its GPU's NUMA node.
+
+    Call before allocating pinned host buffers: cudaHostAlloc first-touches its
+    pages from the calling thread, so they then live on the GPU's node and the
+    per-step H2D/D2H copies do not cross the socket interconnect. Returns
+    {"node", "cpus"} (node None and every allowed CPU when the topology is
+    unknown or has a single node).
+    """
+    allowed = os.sched_getaffinity(0)
+    node = gpu_numa_node(device)
+    if node is None:
+        return {"node": None, "cpus": len(allowed)}
+    try:
+        cpus = _cpulist(open(f"/sys/devices/system/node/node{node}/cpulist").read()) & allowed
+    except OSError:
+        cpus = set()
+    if cpus:
+        os.sched_setaffinity(0, cpus)
+    return {"node": node, "cpus": len(cpus) or len(allowed)}
+
+
 def rank_sizes(n_local: int, group=None, device=None) -> list[int]:
     """Every rank's leading (env) size, in rank order (one small all_gather)."""
     world = dist.get_world_size(group)
@@ -252,6 +295,7 @@ class PeerFrameSink:
                 p = ctypes.c_void_p()
                 _native.check(lib.mdrt_peer_open(dev, h, ctypes.byref(p)))
                 self._mapped.append(p.value)
+                _native.register_remote(p.value, nbytes)   # renders into it use MDRT_WIDE_STORES
             bases = list(self._mapped)
         self._local = [wrap_pointer(b + self.off, (self.env_count,) + self.per_env, self.device, self._keep)
                        for b in bases]
@@ -286,6 +330,7 @@ class PeerFrameSink:
         torch.cuda.synchronize(self.device)
         self._local, self._full = [], None
         for p in self._mapped:
+            self._native.unregister_remote(p)
             self._native.check(lib.mdrt_peer_close(ctypes.c_void_p(p)))
         if self.world > 1:
             dist.barrier(group=self.group)   # every mapping closed before the owner frees

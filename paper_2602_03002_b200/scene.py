@@ -369,6 +369,8 @@ class Scene:
             a.fov_delta = self._rand_fov.data_ptr()
         a.ray_envs = 1
         a.out = out.data_ptr()
+        if _native.is_remote(a.out):
+            a.flags |= _native.WIDE_STORES
         return a
 
     def _launch(self, args: _native.StepArgs) -> None:

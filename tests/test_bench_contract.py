@@ -1,6 +1,10 @@
 """bench.py contract on CPU: the reference arm's JSON line (keys, units, the
-cpu_baseline and e2e objects) and its torchrun behaviour (non-zero ranks exit
-silently). The GPU arm is exercised on the B200 by the driver."""
+cpu_baseline and e2e objects; the live reference from baseline/_ref and the C
+port), its torchrun behaviour (non-zero ranks exit silently) and the launcher's
+hard failures (--gpus N without N GPUs, WORLD_SIZE != --gpus). The GPU arm is
+exercised on the B200 (tests/test_gpu_bench.py and the driver)."""
+
+import pytest
 
 import json
 import os
@@ -10,12 +14,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(extra_env=None):
+def _run(extra_env=None, extra_args=("--ref-impl", "port", "--cpu-seconds", "0.3"), rc=0):
     env = dict(os.environ, **(extra_env or {}))
     res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--warmup", "1", "--cpu-seconds", "0.3"], capture_output=True, text=True, env=env,
+                          "--warmup", "1", *extra_args], capture_output=True, text=True, env=env,
                          timeout=600, cwd=ROOT)
-    assert res.returncode == 0, res.stderr[-2000:]
+    assert res.returncode == rc, res.stderr[-2000:]
     return [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
 
 
@@ -28,7 +32,7 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["unit"] == "rays/s" and d["value"] > 0
     assert d["higher_is_better"] is True and d["scaling"] == "weak" and d["vs_baseline"] is None
-    assert "workload" in d["config"]
+    assert {"workload", "envs_per_gpu", "cams", "resolution", "global_envs"} <= set(d["config"])
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert set(cb["split"]) >= {"render_only_mean", "render_plus_sensor_mean"}
@@ -38,4 +42,29 @@ def test_reference_arm_json_line():
 
 
 def test_reference_arm_nonzero_rank_is_silent():
-    assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}) == []
+    assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"},
+                extra_args=("--gpus", "2", "--ref-impl", "port", "--cpu-seconds", "0.3")) == []
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "multidepth")),
+                    reason="reference not installed in baseline/_ref")
+def test_reference_arm_runs_the_live_reference():
+    d = _run(extra_args=("--envs", "4", "--ref-impl", "live"))[0]
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and "multidepth.render(backend='numba'" in cb["sample"]
+    assert d["config"]["envs_per_gpu"] == 4 and d["value"] > 0
+
+
+def test_launcher_fails_loudly():
+    """--gpus 2 with no (or too few) GPUs and no share mode exits non-zero with a message;
+    a torchrun world that disagrees with --gpus too."""
+    bench = os.path.join(ROOT, "bench.py")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK",
+                                                               "MDRT_BENCH_SHARE_GPU")}
+    res = subprocess.run([sys.executable, bench, "--gpus", "2", "--steps", "1", "--warmup", "1"], capture_output=True,
+                         text=True, env=env, timeout=300, cwd=ROOT)
+    assert res.returncode != 0 and "bench.py:" in res.stderr
+    env.update(RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, bench, "--gpus", "1", "--steps", "1", "--warmup", "1"], capture_output=True,
+                         text=True, env=env, timeout=300, cwd=ROOT)
+    assert res.returncode == 2 and "WORLD_SIZE=2" in res.stderr

@@ -70,6 +70,38 @@ def _host_staging(nbytes: int, device) -> torch.Tensor:
 
 
 _in_staging: dict = {}
+_grid_cache: dict = {}      # device -> [(source array, fingerprint, device tensor)], most recent last
+_GRID_CACHE_SLOTS = 2      # ray_dirs + ray_scale of the current scene
+
+
+def _fingerprint(x: np.ndarray):
+    """Cheap identity of a host array's contents: pointer, shape, strides, dtype and a
+    strided sample of <= 65,536 elements (plus the first and last 64)."""
+    flat = x.reshape(-1)
+    step = max(1, flat.size // 65536)
+    sample = np.concatenate([flat[::step], flat[:64], flat[-64:]])
+    return (x.ctypes.data, x.shape, x.strides, x.dtype.str, hash(sample.tobytes()))
+
+
+def _cached_grid(x, device, slot):
+    """Ray grids are built once by the reference Scene and handed over unchanged on
+    every call (scene.py:304-329); with per-env FOV randomisation they are
+    (N,C,H,W,3) f64, 604 MB at config 2. Keep their device copy and re-upload only
+    when the caller passes a different array or its sampled contents changed."""
+    if isinstance(x, torch.Tensor):
+        return _dev(x, device, slot)
+    x = np.asarray(x)
+    fp = _fingerprint(x)
+    entries = _grid_cache.setdefault(device.index, [])
+    for i, (src, f, t) in enumerate(entries):
+        if src is x and f == fp:
+            entries.append(entries.pop(i))
+            return t
+    t = _dev(x, device, slot).clone()   # own copy: the staging slot is reused by the next upload
+    entries.append((x, fp, t))
+    while len(entries) > _GRID_CACHE_SLOTS:
+        entries.pop(0)
+    return t
 
 
 def _dev(x, device, slot=0):
@@ -111,7 +143,7 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
     b = len(flat.body_root)
     bp, bq = _dev(body_pos, device, 0), _dev(body_rot, device, 1)
     cp, cq = _dev(cam_pos, device, 2), _dev(cam_rot, device, 3)
-    rd, rs = _dev(ray_dirs, device, 4), _dev(ray_scale, device, 5)
+    rd, rs = _cached_grid(ray_dirs, device, 4), _cached_grid(ray_scale, device, 5)
     if tuple(rd.shape[1:]) != (c, h, w, 3) or tuple(rs.shape[1:]) != (c, h, w):
         raise ValueError("ray grids must be shaped (RN,C,H,W,3) / (RN,C,H,W)")
     dev_out = out if isinstance(out, torch.Tensor) and out.is_cuda and out.is_contiguous() else \
@@ -132,11 +164,59 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
         if isinstance(out, torch.Tensor):
             out.copy_(dev_out)
         else:
-            # pinned staging (full PCIe rate), then a multithreaded host copy into the
-            # caller's (typically freshly allocated, scene.py:344-347) numpy array
-            stage = _host_staging(dev_out.numel() * 4, device)[:dev_out.numel() * 4].view(torch.float32)
-            stage = stage.view(dev_out.shape)
-            stage.copy_(dev_out, non_blocking=True)
-            torch.cuda.current_stream(device).synchronize()
-            torch.from_numpy(out).copy_(stage) if out.flags.c_contiguous else np.copyto(out, stage.numpy())
+            _deliver_host(dev_out, out, device)
     return out
+
+
+_CHUNKS = 8
+
+
+def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
+    """Device frame -> the caller's numpy ``out`` (typically freshly allocated,
+    scene.py:344-347, so its pages are first touched here). Chunked pipeline: the
+    PCIe copy of chunk k+1 into pinned staging overlaps the multithreaded host
+    copy of chunk k into ``out``; transparent huge pages are requested for ``out``
+    so first-touch faults are per 2 MB instead of per 4 KB."""
+    n = dev_out.numel()
+    stage = _host_staging(n * 4, device)[:n * 4].view(torch.float32)
+    src = dev_out.reshape(-1)
+    if not out.flags.c_contiguous:
+        stage.copy_(src)
+        np.copyto(out, stage.numpy().reshape(out.shape))
+        return
+    _advise_hugepages(out)
+    dst = torch.from_numpy(out.reshape(-1))
+    bounds = [n * k // _CHUNKS for k in range(_CHUNKS + 1)]
+    cur = torch.cuda.current_stream(device)
+    ready = []
+    for k in range(_CHUNKS):
+        lo, hi = bounds[k], bounds[k + 1]
+        stage[lo:hi].copy_(src[lo:hi], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        ready.append(ev)
+    for k in range(_CHUNKS):
+        lo, hi = bounds[k], bounds[k + 1]
+        ready[k].synchronize()
+        dst[lo:hi].copy_(stage[lo:hi])
+
+
+_MADV_HUGEPAGE = 14
+_libc = None
+
+
+def _advise_hugepages(a: np.ndarray) -> None:
+    global _libc
+    if a.nbytes < (8 << 20):
+        return
+    try:
+        import ctypes
+        if _libc is None:
+            _libc = ctypes.CDLL(None, use_errno=True)
+        page = 1 << 21
+        start = (a.ctypes.data + page - 1) & ~(page - 1)
+        end = (a.ctypes.data + a.nbytes) & ~(page - 1)
+        if end > start:
+            _libc.madvise(ctypes.c_void_p(start), ctypes.c_size_t(end - start), _MADV_HUGEPAGE)
+    except (OSError, AttributeError):
+        pass

@@ -177,10 +177,62 @@ def make_terrain(md):
     np.savez_compressed(os.path.join(HERE, "terrain.npz"), **out)
 
 
+def make_seam(md):
+    """The exact arguments the live reference hands its backend seam: render() is run
+    with get_render_fn wrapped so the numba render_batch call (numba_backend.py:222-234)
+    is recorded -- the real FlatGeometry (median-split forest, leaf-ordered triangles),
+    f64 body/camera poses, the per-env FOV-randomised ray grids, d_max, and the output
+    it wrote (scene.py:332-348)."""
+    from multidepth import kernels as mk
+    from paper_2602_03002_b200 import synth
+    w = synth.config("cfg1", 4)
+    n = 4
+    rng = np.random.default_rng(31)
+    bp, bq = w.poses(0)
+    bp = f32(bp + rng.normal(0.0, 0.05, bp.shape) * np.array([1.0, 1.0, 0.2]))
+    bq = unit_f32(bq)
+    bodies = [(nm, md.TriMesh(f32(m.vertices), m.faces, frame="body-local")) for nm, m in w.bodies]
+    cams = [md.CameraModel(width=c.width, height=c.height, hfov_deg=c.hfov_deg, vfov_deg=c.vfov_deg, d_max=c.d_max,
+                           mount=md.RigidPose(c.mount.translation, c.mount.rotation), parent_body=c.parent_body)
+            for c in synth.torso_cameras(2)]
+    scene = md.Scene(num_envs=n, bodies=bodies, cameras=cams,
+                     terrain=md.TriMesh(f32(w.terrain.mesh.vertices), w.terrain.mesh.faces))
+    scene.set_body_poses(bp, bq)
+    po, ro, fo = md.sample_camera_offsets(md.CameraRandomization(seed=5), n, 2)
+    scene.set_camera_randomization(f32(po), unit_f32(ro), f32(fo))
+    captured = {}
+    real = mk.get_render_fn
+
+    def spy(backend=None):
+        name, fn = real(backend)
+
+        def rec(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max, early, out, threads):
+            fn(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max, early, out, threads)
+            for f in ("body_root", "node_min", "node_max", "left", "right", "start", "count", "tri_v0", "tri_v1",
+                      "tri_v2", "body_tri_offsets", "g_node_min", "g_node_max", "g_left", "g_right", "g_start",
+                      "g_count", "g_tri_v0", "g_tri_v1", "g_tri_v2"):
+                captured["flat_" + f] = np.asarray(getattr(flat, f)).copy()
+            captured.update(body_pos=np.array(body_pos), body_rot=np.array(body_rot), cam_pos=np.array(cam_pos),
+                            cam_rot=np.array(cam_rot), ray_dirs=np.array(ray_dirs), ray_scale=np.array(ray_scale),
+                            d_max=np.array(d_max), early=np.array(bool(early)), out=out.copy())
+        return name, rec
+
+    mk.get_render_fn = spy
+    try:
+        frame = md.render(scene, backend="numba")
+    finally:
+        mk.get_render_fn = real
+    assert np.array_equal(frame.data, captured["out"])
+    np.savez_compressed(os.path.join(HERE, "seam_capture.npz"), **captured)
+    print("seam", captured["out"].shape, "ray_dirs", captured["ray_dirs"].shape,
+          "hits", int((captured["out"] < 10.0).sum()))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=os.environ.get("MULTIDEPTH_REF", "/root/reference/pkg/src"))
-    ap.add_argument("--only", choices=["frameio", "terrain"], default=None, help="regenerate one fixture group")
+    ap.add_argument("--only", choices=["frameio", "terrain", "seam"], default=None,
+                    help="regenerate one fixture group")
     args = ap.parse_args()
     os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_cache_golden"))
     sys.dont_write_bytecode = True
@@ -194,6 +246,8 @@ def main():
         make_frameio(md)
     if args.only in (None, "terrain"):
         make_terrain(md)
+    if args.only in (None, "seam"):
+        make_seam(md)
     if args.only is not None:
         print("done")
         return

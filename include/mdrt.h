@@ -262,6 +262,13 @@ int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_
  * float per block into `sink` (device, >= 4096 floats) so loads are live. */
 int mdrt_probe_read(const void *buf, int64_t bytes, int32_t iters, float *sink, void *stream);
 
+/* Fault in a HOST buffer's pages from `threads` threads (one write per 4 KB page,
+ * values unchanged). The reference's render() hands its backend a freshly
+ * allocated numpy `out` (scene.py:344-347); touching it while the GPU renders
+ * takes the first-touch page faults off the critical path of the device->host
+ * copy into it (kernels/cuda_backend.py). */
+int mdrt_host_touch(void *ptr, int64_t bytes, int32_t threads);
+
 /* Fused frame gather over peer memory (the reference
  * has no multi-GPU path, its closest interface is the caller-allocated `out`
  * of render_batch, numba_backend.py:222-234). The destination rank allocates

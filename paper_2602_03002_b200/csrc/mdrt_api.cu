@@ -12,6 +12,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mdrt.h"
@@ -840,6 +841,31 @@ int mdrt_probe_read(const void* buf, int64_t bytes, int32_t iters, float* sink, 
         need(buf && sink && bytes >= 16 && iters >= 1, "bad probe arguments");
         launch_probe_read(static_cast<const float4*>(buf), bytes / 16, iters, sink, static_cast<cudaStream_t>(stream));
         CK(cudaGetLastError());
+    });
+}
+
+int mdrt_host_touch(void* ptr, int64_t bytes, int32_t threads) {
+    return guarded([&] {
+        need(ptr != nullptr || bytes == 0, "ptr is NULL");
+        need(bytes >= 0 && threads >= 1 && threads <= 256, "bad host_touch arguments");
+        if (bytes == 0) return;
+        // one write per 4 KB page; threads take contiguous slices (page faults on
+        // different ranges of one mapping proceed in parallel)
+        constexpr int64_t kPage = 4096;
+        volatile char* base = static_cast<volatile char*>(ptr);
+        const int64_t pages = (bytes + kPage - 1) / kPage;
+        const int n = static_cast<int>(std::min<int64_t>(threads, std::max<int64_t>(1, pages / 64)));
+        auto work = [&](int t) {
+            const int64_t lo = pages * t / n, hi = pages * (t + 1) / n;
+            for (int64_t p = lo; p < hi; ++p) {
+                const int64_t off = std::min(p * kPage, bytes - 1);
+                base[off] = base[off];
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < n; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
     });
 }
 

@@ -14,7 +14,10 @@ cross the boundary.
 
 from __future__ import annotations
 
+import os
+import sys
 import threading
+import time
 
 import numpy as np
 import torch
@@ -75,11 +78,16 @@ _GRID_CACHE_SLOTS = 2      # ray_dirs + ray_scale of the current scene
 
 
 def _fingerprint(x: np.ndarray):
-    """Cheap identity of a host array's contents: pointer, shape, strides, dtype and a
-    strided sample of <= 65,536 elements (plus the first and last 64)."""
+    """Cheap identity of a host array's contents: pointer, shape, strides, dtype and
+    256 evenly spaced runs of 64 contiguous elements (whole arrays up to 16,384
+    elements). Runs, not single strided elements: a 604 MB grid is sampled through
+    256 cache/TLB misses instead of 65,536."""
     flat = x.reshape(-1)
-    step = max(1, flat.size // 65536)
-    sample = np.concatenate([flat[::step], flat[:64], flat[-64:]])
+    if flat.size <= 16384:
+        sample = flat
+    else:
+        starts = np.linspace(0, flat.size - 64, 256).astype(np.int64)
+        sample = flat[(starts[:, None] + np.arange(64)[None, :]).ravel()]
     return (x.ctypes.data, x.shape, x.strides, x.dtype.str, hash(sample.tobytes()))
 
 
@@ -137,6 +145,17 @@ def render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale
 def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scale, d_max,
                   early_termination, out):
     n, c, h, w = out.shape
+    tm = [time.perf_counter()] if _TIMING else None
+    host_np = isinstance(out, np.ndarray)
+    mapped = host_np and _MODE == "mapped" and out.flags.c_contiguous
+    toucher = None
+    if mapped and _TOUCH and _CONC:
+        # fault in the caller's fresh pages on other cores while this thread uploads the
+        # inputs and the GPU renders (the ctypes call releases the GIL)
+        _advise_hugepages(out)
+        toucher = threading.Thread(target=_native.lib().mdrt_host_touch,
+                                   args=(out.ctypes.data, out.nbytes, _touch_threads()))
+        toucher.start()
     device = out.device if isinstance(out, torch.Tensor) and out.is_cuda else _cuda_device(None)
     d_max = np.broadcast_to(np.asarray(d_max, np.float64), (c,))
     ctx = _context(flat, c, h, w, d_max, device)
@@ -146,11 +165,18 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
     rd, rs = _cached_grid(ray_dirs, device, 4), _cached_grid(ray_scale, device, 5)
     if tuple(rd.shape[1:]) != (c, h, w, 3) or tuple(rs.shape[1:]) != (c, h, w):
         raise ValueError("ray grids must be shaped (RN,C,H,W,3) / (RN,C,H,W)")
-    dev_out = out if isinstance(out, torch.Tensor) and out.is_cuda and out.is_contiguous() else \
-        torch.empty((n, c, h, w), dtype=torch.float32, device=device)
+    if mapped:
+        # the kernel stores straight into pinned host memory (UVA-mapped): the PCIe
+        # transfer overlaps the traversal instead of following it
+        dev_out = _host_staging(out.nbytes, device)[:out.nbytes].view(torch.float32).view(n, c, h, w)
+    else:
+        dev_out = out if isinstance(out, torch.Tensor) and out.is_cuda and out.is_contiguous() else \
+            torch.empty((n, c, h, w), dtype=torch.float32, device=device)
     a = _native.StepArgs()
     a.num_envs = n
     a.flags = _native.EARLY_TERMINATION if early_termination else 0
+    if mapped:
+        a.flags |= _native.WIDE_STORES       # 32 B row segments per PCIe write
     a.body_pos = bp.data_ptr() if b else None
     a.body_rot = bq.data_ptr() if b else None
     a.cam_pos = cp.data_ptr()
@@ -159,7 +185,26 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
     a.ray_scale = rs.data_ptr()
     a.ray_envs = int(rd.shape[0])
     a.out = dev_out.data_ptr()
+    if tm:
+        tm.append(time.perf_counter())
     ctx.render(a, torch.cuda.current_stream(device).cuda_stream)
+    if mapped:
+        if toucher is not None:
+            toucher.join()
+        elif _TOUCH:
+            _advise_hugepages(out)
+            _native.check(_native.lib().mdrt_host_touch(out.ctypes.data, out.nbytes, _touch_threads()))
+        if tm:
+            tm.append(time.perf_counter())
+        torch.cuda.current_stream(device).synchronize()
+        if tm:
+            tm.append(time.perf_counter())
+        torch.from_numpy(out.reshape(-1)).copy_(dev_out.reshape(-1))
+        if tm:
+            tm.append(time.perf_counter())
+            print("seam ms: inputs %.2f touch %.2f wait %.2f copy %.2f" % tuple(
+                1e3 * (b - a_) for a_, b in zip(tm, tm[1:])), file=sys.stderr)
+        return out
     if dev_out is not out:
         if isinstance(out, torch.Tensor):
             out.copy_(dev_out)
@@ -184,7 +229,8 @@ def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
         stage.copy_(src)
         np.copyto(out, stage.numpy().reshape(out.shape))
         return
-    _advise_hugepages(out)
+    if _TOUCH:
+        _advise_hugepages(out)
     dst = torch.from_numpy(out.reshape(-1))
     bounds = [n * k // _CHUNKS for k in range(_CHUNKS + 1)]
     cur = torch.cuda.current_stream(device)
@@ -195,10 +241,34 @@ def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
         ev = torch.cuda.Event()
         ev.record(cur)
         ready.append(ev)
+    if _TOUCH:
+        # fault in the caller's fresh pages while the GPU renders and copies
+        _native.check(_native.lib().mdrt_host_touch(out.ctypes.data, out.nbytes, _touch_threads()))
     for k in range(_CHUNKS):
         lo, hi = bounds[k], bounds[k + 1]
         ready[k].synchronize()
         dst[lo:hi].copy_(stage[lo:hi])
+
+
+_TOUCH = os.environ.get("MDRT_SEAM_TOUCH", "1") != "0"    # A/B knobs (tools/seam_profile.py)
+# Seam output delivery into the caller's fresh numpy `out` (config 2, 100 MB, per call,
+# medians on a 16-core B200 host, profiles/experiments/r02_seam_delivery.txt):
+#   stage  (kernel -> device out -> 8 chunked D2H -> copy)              ~9.3 ms
+#   mapped (kernel stores into pinned host memory over PCIe -> copy)    ~8.2 ms
+# with the fresh pages faulted in by 16 threads while the GPU works (first-touch
+# zeroing of 100 MB costs ~4 ms on that host and is the largest single part).
+_MODE = os.environ.get("MDRT_SEAM_MODE", "mapped")       # mapped | stage
+_TIMING = os.environ.get("MDRT_SEAM_TIMING") == "1"
+_CONC = os.environ.get("MDRT_SEAM_TOUCH_CONC", "0") == "1"
+
+
+def _touch_threads() -> int:
+    if os.environ.get("MDRT_SEAM_TOUCH_THREADS"):
+        return int(os.environ["MDRT_SEAM_TOUCH_THREADS"])
+    try:
+        return max(1, min(16, len(os.sched_getaffinity(0))))
+    except AttributeError:
+        return 8
 
 
 _MADV_HUGEPAGE = 14

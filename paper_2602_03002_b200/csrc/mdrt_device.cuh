@@ -464,7 +464,8 @@ struct Traversal {
             const bool h1 = c1min <= c1max;
             if (h0 && h1) {
                 const bool swap = c1min < c0min;
-                push(make_int2(swap ? rf.x : rf.y, __float_as_int(swap ? c0min : c1min)));
+                const int32_t far = swap ? rf.x : rf.y;
+                push(make_int2(far, __float_as_int(swap ? c0min : c1min)));
                 ref = swap ? rf.y : rf.x;
             } else if (h0 || h1) {
                 ref = h0 ? rf.x : rf.y;

@@ -524,6 +524,8 @@ def ours(args):
     t_build = time.perf_counter()
     scene = md.Scene(n, bodies=bodies, cameras=w.cameras, terrain=terrain, device=dev, env_offset=env0)
     t_build = time.perf_counter() - t_build
+    if os.environ.get("MDRT_NO_TILE_ENTRY") == "1":      # A/B: terrain traversal from the root
+        scene.debug_flags |= _native.NO_TILE_ENTRY
     C, H, W = scene.num_cameras, scene.height, scene.width
     rays_per_step = n * C * H * W
 
@@ -905,7 +907,8 @@ def ours(args):
                                  else "full observation (N,C,H,W) f32",
                     "how": "pinned-host poses H2D (upload stream) + fused pipeline + result D2H (copy stream, "
                            "double-buffered) every step, L2 flush inside the timed loop, events around the whole loop"},
-            "gpu_launches": 2 * args.steps,
+            # prologue + per-tile entry kernel + render kernel per step
+            "gpu_launches": (2 if scene.debug_flags & _native.NO_TILE_ENTRY else 3) * args.steps,
             "graph": {"value": all_rays / (graph_ms * 1e-3), "unit": "rays/s", "ms_per_step": graph_ms / args.steps,
                       "how": "CapturedStep replay (advance+prologue+render CUDA graph, device step state), "
                              "device pose copy + L2 flush between steps as for value"},

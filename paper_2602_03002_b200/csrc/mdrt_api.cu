@@ -5,6 +5,7 @@
 // the device; afterwards only per-step pose/camera/sensor data flows in.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -138,6 +139,7 @@ struct mdrt_ctx {
         return tri_tex;
     }
     DevBuf<int2> rects;
+    DevBuf<int32_t> tile_entry;   // per-tile terrain entry refs (prologue -> render kernel)
     DevBuf<unsigned int> tile_counter;
     DevBuf<StepState> state;
     // Cross-stream ordering of the per-step scratch (views, links, rects, tile
@@ -165,6 +167,11 @@ struct mdrt_ctx {
         return st != cudaStreamCaptureStatusNone;
     }
 };
+
+namespace {
+int tiles_per_view_for(int W, int H, int tw) { return ((W + tw - 1) / tw) * ((H + 32 / tw - 1) / (32 / tw)); }
+int max_tiles_per_view(int W, int H) { return std::max(tiles_per_view_for(W, H, 4), tiles_per_view_for(W, H, 8)); }
+}  // namespace
 
 extern "C" {
 
@@ -209,6 +216,7 @@ int mdrt_destroy(mdrt_ctx* ctx) {
         ctx->views.release();
         ctx->links.release();
         ctx->rects.release();
+        ctx->tile_entry.release();
         ctx->tile_counter.release();
         ctx->state.release();
         if (ctx->done) cudaEventDestroy(ctx->done);
@@ -462,6 +470,27 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         pp.views = ctx->views.ptr;
         pp.links = ctx->links.ptr;
         pp.rects = ctx->rects.ptr;
+        // tile shape of this call (the prologue computes per-tile terrain entries for it)
+        const int tile_w = (a->flags & MDRT_WIDE_STORES) ? 8 : render_tile_width(ctx->W);
+        const int tile_h = 32 / tile_w;
+        const int tiles_x = (ctx->W + tile_w - 1) / tile_w;
+        const int tiles_per_view = tiles_x * ((ctx->H + tile_h - 1) / tile_h);
+        const bool entries = ctx->has_terrain && !pp.grid_mode && !(a->flags & MDRT_NO_TILE_ENTRY);
+        EntryParams ep{};
+        if (entries) {
+            ctx->tile_entry.reserve(std::max<size_t>(1, nviews * max_tiles_per_view(ctx->W, ctx->H)));
+            ep.views = ctx->views.ptr;
+            ep.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);
+            ep.root = ctx->terrain_root;
+            ep.W = ctx->W;
+            ep.H = ctx->H;
+            ep.tile_w = tile_w;
+            ep.tile_h = tile_h;
+            ep.tiles_x = tiles_x;
+            ep.tiles_per_view = tiles_per_view;
+            ep.views_count = static_cast<int64_t>(nviews);
+            ep.out = ctx->tile_entry.ptr;
+        }
         ctx->tile_counter.reserve(kTileCounters);
         pp.reset_counter = ctx->tile_counter.ptr;
         pp.reset_count = kTileCounters;
@@ -474,6 +503,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         if (!only_trace) {
             launch_prologue(pp, static_cast<int64_t>(nviews), s);
             CK(cudaGetLastError());
+            if (entries) {
+                launch_entry(ep, s);
+                CK(cudaGetLastError());
+            }
         }
         if (only_pro) {
             if (ordered) ctx->order_end(s);
@@ -483,10 +516,10 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         RenderParams rp{};
         rp.N = N; rp.C = C; rp.B = B; rp.W = ctx->W; rp.H = ctx->H;
         // remote `out` (fused gather over NVLink): 8-wide tiles, 32 B contiguous per row store
-        rp.tile_w = (a->flags & MDRT_WIDE_STORES) ? 8 : render_tile_width(ctx->W);
-        const int tile_h = 32 / rp.tile_w;
-        rp.tiles_x = (ctx->W + rp.tile_w - 1) / rp.tile_w;
-        rp.tiles_per_view = rp.tiles_x * ((ctx->H + tile_h - 1) / tile_h);
+        rp.tile_w = tile_w;
+        rp.tiles_x = tiles_x;
+        rp.tiles_per_view = tiles_per_view;
+        rp.tile_entry = entries ? ctx->tile_entry.ptr : nullptr;
         rp.m_tiles_x = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_x));
         rp.m_tiles_per_view = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_per_view));
         rp.m_C = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(C));
@@ -591,6 +624,7 @@ int mdrt_state_set(mdrt_ctx* ctx, int32_t num_envs, uint64_t sensor_key, uint64_
         ctx->views.reserve(nviews);
         ctx->links.reserve(std::max<size_t>(1, nviews * std::max<size_t>(ctx->bodies.size(), 1)));
         ctx->rects.reserve(std::max<size_t>(1, nviews * std::max<size_t>(ctx->bodies.size(), 1)));
+        ctx->tile_entry.reserve(std::max<size_t>(1, nviews * max_tiles_per_view(ctx->W, ctx->H)));
         ctx->tile_counter.reserve(kTileCounters);
         CK(cudaMemcpy(ctx->state.ptr, &st, sizeof(st), cudaMemcpyHostToDevice));
     });

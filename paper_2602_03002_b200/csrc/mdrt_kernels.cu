@@ -84,6 +84,116 @@ __device__ __forceinline__ void load_pose(const PrologueParams& p, int64_t e, in
 }
 
 // ---------------------------------------------------------------------------
+// Per-tile terrain entry nodes. Every ray of a pixel tile lies inside the tile's
+// view pyramid: apex at the camera, side planes through the tile's corner
+// pixel-centre rays, far plane at camera depth d_max (a ray's range is at most
+// d_max, so its camera-frame depth is too). Descending the terrain BVH from the
+// root while only one child box meets the pyramid (1 cm margin) reaches a node
+// every ray of the tile would reach first anyway: a ray's own slab test can only
+// enter a box its segment meets, and the skipped siblings are >= 1 cm from every
+// ray, far beyond the fp32 error of the slab and triangle tests. Starting there
+// yields the identical closest hit while the coherent top-level node fetches
+// (all 32 lanes reading the same records) are done once per tile by one lane of
+// the prologue instead of once per ray.
+// ---------------------------------------------------------------------------
+struct TilePyramid {
+    float lo[3], hi[3];   // AABB of the apex and the far corners
+    float n[6][3], d[6];  // planes n.p + d >= 0 contain the pyramid (unit n)
+};
+
+__device__ __forceinline__ void pyramid_setup(TilePyramid& f, const float R[9], const float o[3], float u0, float u1,
+                                              float v0, float v1, float far) {
+    const float cu[4] = {u0, u1, u1, u0}, cv[4] = {v0, v0, v1, v1};
+    float D[4][3];
+    for (int k = 0; k < 4; ++k) {
+        D[k][0] = R[0] * cu[k] + R[1] * cv[k] + R[2];
+        D[k][1] = R[3] * cu[k] + R[4] * cv[k] + R[5];
+        D[k][2] = R[6] * cu[k] + R[7] * cv[k] + R[8];
+    }
+    for (int a = 0; a < 3; ++a) {
+        f.lo[a] = o[a];
+        f.hi[a] = o[a];
+        for (int k = 0; k < 4; ++k) {
+            const float q = o[a] + far * D[k][a];
+            f.lo[a] = fminf(f.lo[a], q);
+            f.hi[a] = fmaxf(f.hi[a], q);
+        }
+    }
+    for (int k = 0; k < 4; ++k) {
+        const float* A = D[k];
+        const float* B = D[(k + 1) & 3];
+        const float* Cn = D[(k + 2) & 3];
+        float nx = A[1] * B[2] - A[2] * B[1], ny = A[2] * B[0] - A[0] * B[2], nz = A[0] * B[1] - A[1] * B[0];
+        const float inv = rsqrtf(fmaxf(nx * nx + ny * ny + nz * nz, 1e-30f));
+        nx *= inv; ny *= inv; nz *= inv;
+        if (nx * Cn[0] + ny * Cn[1] + nz * Cn[2] < 0.f) { nx = -nx; ny = -ny; nz = -nz; }
+        f.n[k][0] = nx; f.n[k][1] = ny; f.n[k][2] = nz;
+        f.d[k] = -(nx * o[0] + ny * o[1] + nz * o[2]);
+    }
+    const float fx = R[2], fy = R[5], fz = R[8];   // camera +z (forward) in world
+    const float fo = fx * o[0] + fy * o[1] + fz * o[2];
+    f.n[4][0] = fx; f.n[4][1] = fy; f.n[4][2] = fz; f.d[4] = -fo;            // in front of the camera
+    f.n[5][0] = -fx; f.n[5][1] = -fy; f.n[5][2] = -fz; f.d[5] = fo + far;    // within depth d_max
+}
+
+// true when the box certainly misses the pyramid (separated by its AABB or a plane)
+__device__ __forceinline__ bool pyramid_misses(const TilePyramid& f, float lx, float hx, float ly, float hy, float lz,
+                                               float hz) {
+    constexpr float eps = 0.01f;
+    if (!(lx <= f.hi[0] + eps && hx >= f.lo[0] - eps && ly <= f.hi[1] + eps && hy >= f.lo[1] - eps &&
+          lz <= f.hi[2] + eps && hz >= f.lo[2] - eps))
+        return true;   // also empty boxes (lo = +inf, hi = -inf)
+    const float cx = 0.5f * (lx + hx), cy = 0.5f * (ly + hy), cz = 0.5f * (lz + hz);
+    const float ex = 0.5f * (hx - lx), ey = 0.5f * (hy - ly), ez = 0.5f * (hz - lz);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const float* n = f.n[k];
+        const float reach = n[0] * cx + n[1] * cy + n[2] * cz + fabsf(n[0]) * ex + fabsf(n[1]) * ey +
+                            fabsf(n[2]) * ez + f.d[k];
+        if (reach < -eps) return true;
+    }
+    return false;
+}
+
+// descend from the terrain root while exactly one child meets the pyramid: the
+// entry ref (inner node, leaf, or kExit when no terrain box meets it)
+__device__ int32_t pyramid_entry(const float4* __restrict__ nodes, int32_t root, const TilePyramid& f) {
+    int32_t ref = root;
+    for (int lvl = 0; lvl <= kStack + 1 && ref >= 0; ++lvl) {
+        const float4* n = nodes + 4 * static_cast<int64_t>(ref);
+        const float4 bx = __ldg(n), by = __ldg(n + 1), bz = __ldg(n + 2);
+        const int2 rf = __ldg(reinterpret_cast<const int2*>(n + 3));
+        const bool m0 = pyramid_misses(f, bx.x, bx.y, bx.z, bx.w, bz.x, bz.y);
+        const bool m1 = pyramid_misses(f, by.x, by.y, by.z, by.w, bz.z, bz.w);
+        if (!m0 && !m1) break;
+        if (m0 && m1) return kExit;
+        ref = m0 ? rf.y : rf.x;
+    }
+    return ref;
+}
+
+// One thread per (view, tile), after the prologue wrote the view records (the
+// render kernel's own f32 camera rotation, origin and intrinsics).
+static __global__ void __launch_bounds__(128) entry_kernel(EntryParams p) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.views_count * p.tiles_per_view) return;
+    const int64_t view = i / p.tiles_per_view;
+    const int tl = static_cast<int>(i - view * p.tiles_per_view);
+    const ViewRec& V = p.views[view];
+    float R[9], o[3];
+    for (int k = 0; k < 9; ++k) R[k] = V.r[k];
+    for (int k = 0; k < 3; ++k) o[k] = V.o[k];
+    const int ty = tl / p.tiles_x, tx = tl - ty * p.tiles_x;
+    const int x0 = tx * p.tile_w, x1 = min(x0 + p.tile_w, p.W) - 1;
+    const int y0 = ty * p.tile_h, y1 = min(y0 + p.tile_h, p.H) - 1;
+    constexpr float m = 1e-4f;   // direction margin (tangent units) over the f32 rounding of u, v
+    TilePyramid f;
+    pyramid_setup(f, R, o, fmaf(static_cast<float>(x0), V.ax, V.bx) - m, fmaf(static_cast<float>(x1), V.ax, V.bx) + m,
+                  fmaf(static_cast<float>(y0), V.ay, V.by) - m, fmaf(static_cast<float>(y1), V.ay, V.by) + m, V.dmax);
+    p.out[i] = pyramid_entry(p.nodes, p.root, f);
+}
+
+// ---------------------------------------------------------------------------
 // K4 prologue: one warp per (env, cam); lanes walk the links.
 // ---------------------------------------------------------------------------
 #ifndef MDRT_PRO_MINB
@@ -426,11 +536,15 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const float wdy = r0.w * dcx + r1.x * dcy + r1.y * dcz;
         const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
         const float bound = p.early_termination ? z : dmax;
+        // the prologue's entry node of this tile (a node every ray of the tile reaches first)
+        const int32_t troot = p.tile_entry ? p.tile_entry[view * static_cast<uint32_t>(p.tiles_per_view) +
+                                                          ty * static_cast<uint32_t>(p.tiles_x) + tx]
+                                           : p.terrain_root;
 #ifdef MDRT_NO_OCTANT
-        const float tt = trace<COUNT>(p.nodes, p.tri_tex, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
+        const float tt = trace<COUNT>(p.nodes, p.tri_tex, troot, r2.y, r2.z, r2.w, wdx, wdy, wdz,
                                       bound * inv_m, stack, ctr, p.n_nodes, p.n_tris);
 #else
-        const float tt = trace_oct<COUNT>(p.nodes, p.tri_tex, p.terrain_root, r2.y, r2.z, r2.w, wdx, wdy, wdz,
+        const float tt = trace_oct<COUNT>(p.nodes, p.tri_tex, troot, r2.y, r2.z, r2.w, wdx, wdy, wdz,
                                           bound * inv_m, stack, ctr, p.n_nodes, p.n_tris);
 #endif
         const float cand = m * tt;
@@ -857,6 +971,10 @@ static unsigned grid_for(int64_t threads, int block) {
 
 void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s) {
     prologue_kernel<<<grid_for(views * 32, 128), 128, 0, s>>>(p);
+}
+
+void launch_entry(const EntryParams& p, cudaStream_t s) {
+    entry_kernel<<<grid_for(p.views_count * p.tiles_per_view, 128), 128, 0, s>>>(p);
 }
 
 int render_tile_width(int W) {

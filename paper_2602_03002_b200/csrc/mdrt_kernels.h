@@ -65,6 +65,17 @@ struct PrologueParams {
     unsigned long long hr_step;   // absorb(rsm key, step)
 };
 
+// Per-tile terrain entry nodes (entry_kernel): the deepest terrain-BVH node whose
+// sibling subtrees all lie outside the pixel tile's view pyramid.
+struct EntryParams {
+    const ViewRec* views;
+    const float4* nodes;          // packed BVH records (terrain tree at root)
+    int32_t root;
+    int32_t W, H, tile_w, tile_h, tiles_x, tiles_per_view;
+    int64_t views_count;          // N * C
+    int32_t* out;                 // (N*C, tiles_per_view) entry refs
+};
+
 struct RenderParams {
     int32_t N, C, B, W, H;
     int32_t tile_w;               // tile shape: tile_w x (32 / tile_w) pixels (4 or 8)
@@ -75,6 +86,7 @@ struct RenderParams {
     uint32_t order_d1, order_m1;  // first divisor of the tile decode (row_tiles or tiles_per_view) + multiplier
     int32_t early_termination;
     int32_t terrain_root;
+    const int32_t* tile_entry;    // per-tile terrain entry refs from the prologue, or NULL (root)
     const float4* nodes;
     const float4* tris;
     int32_t n_nodes, n_tris;      // record counts (bounds of the MDRT_CHECKS build)
@@ -161,6 +173,7 @@ struct DownsampleParams {
 
 // Host-side launchers (defined next to the kernels so templates instantiate there).
 void launch_prologue(const PrologueParams& p, int64_t views, cudaStream_t s);
+void launch_entry(const EntryParams& p, cudaStream_t s);
 // geometry_bytes: BVH node + triangle bytes; above the L2 size the tiles are
 // scheduled SM-locally (render_kernel) so node reuse comes from L1.
 // query_bvh (bvh.py:189-217): closest hit + face of independent rays against one tree

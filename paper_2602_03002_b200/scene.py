@@ -143,6 +143,7 @@ class Scene:
         # CapturedStep recorded against the old pointers refuses to replay
         self._ptr_version = 0
         self._state_owner = None       # the CapturedStep that owns the device step state
+        self.debug_flags = 0           # extra MDRT_* flags for A/B runs (e.g. _native.NO_TILE_ENTRY)
         self.d_max_per_camera = np.array([c.d_max for c in cams], dtype=np.float64)
 
     # -- sizes -------------------------------------------------------------
@@ -351,7 +352,7 @@ class Scene:
     def _step_args(self, out: torch.Tensor, early_termination: bool) -> _native.StepArgs:
         a = _native.StepArgs()
         a.num_envs = self.num_envs
-        a.flags = _native.EARLY_TERMINATION if early_termination else 0
+        a.flags = (_native.EARLY_TERMINATION if early_termination else 0) | self.debug_flags
         a.env_offset = self.env_offset
         a.body_pos = self.body_positions.data_ptr() if self.num_bodies else None
         a.body_rot = self.body_rotations.data_ptr() if self.num_bodies else None

@@ -140,7 +140,7 @@ def test_bench_two_ranks_share_mode():
 
 def test_bench_single_gpu_line():
     d = _line(_bench(["--steps", "3", "--warmup", "3", "--envs", "256", "--cpu-seconds", "2", "--parity-envs", "64"]))
-    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 6
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 9
     r = d["roofline"]
     assert r["bound"] == "l2" and r["peak"] == r["l2_probe_gbs"] and 0 < r["frac"] < 1.5
     p = d["parity"]

@@ -908,7 +908,8 @@ def ours(args):
                     "how": "pinned-host poses H2D (upload stream) + fused pipeline + result D2H (copy stream, "
                            "double-buffered) every step, L2 flush inside the timed loop, events around the whole loop"},
             # prologue + per-tile entry kernel + render kernel per step
-            "gpu_launches": (2 if scene.debug_flags & _native.NO_TILE_ENTRY else 3) * args.steps,
+            "gpu_launches": (2 if (scene.debug_flags & _native.NO_TILE_ENTRY or
+                                   scene.geometry_stats["terrain_triangles"] < 65536) else 3) * args.steps,
             "graph": {"value": all_rays / (graph_ms * 1e-3), "unit": "rays/s", "ms_per_step": graph_ms / args.steps,
                       "how": "CapturedStep replay (advance+prologue+render CUDA graph, device step state), "
                              "device pose copy + L2 flush between steps as for value"},

@@ -48,8 +48,10 @@ extern "C" {
 #define MDRT_WIDE_STORES 0x800    /* `out` is remote (peer-mapped) memory: render 8-pixel-wide tiles so each
                                      warp's obs stores cover >= 32 contiguous bytes per image row (NVLink
                                      writes in whole sectors instead of 16 B pieces)                      */
-#define MDRT_NO_TILE_ENTRY 0x1000 /* A/B: trace the terrain from its root instead of each pixel tile's entry
-                                     node (the prologue's frustum descent; results are identical)         */
+#define MDRT_NO_TILE_ENTRY 0x1000 /* trace the terrain from its root instead of each pixel tile's entry node
+                                     (entry_kernel's frustum descent; results are identical). Neither this
+                                     nor MDRT_TILE_ENTRY: entries when the terrain has >= 65,536 triangles */
+#define MDRT_TILE_ENTRY 0x2000    /* per-tile terrain entry nodes regardless of the terrain size          */
 #define MDRT_DEVICE_STATE 0x100    /* step, timestamp, RNG prefix and ring push come from the context's device
                                       state (mdrt_state_set), advanced on the device at the start of the call:
                                       the call is then CUDA-graph capturable and replayable with no host args */

@@ -34,6 +34,7 @@ RSM = 0x200
 ROT_XYZW = 0x400
 WIDE_STORES = 0x800
 NO_TILE_ENTRY = 0x1000
+TILE_ENTRY = 0x2000
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)

@@ -475,7 +475,12 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         const int tile_h = 32 / tile_w;
         const int tiles_x = (ctx->W + tile_w - 1) / tile_w;
         const int tiles_per_view = tiles_x * ((ctx->H + tile_h - 1) / tile_h);
-        const bool entries = ctx->has_terrain && !pp.grid_mode && !(a->flags & MDRT_NO_TILE_ENTRY);
+        // per-tile entry nodes pay for their extra launch on deep terrain trees (config 2
+        // +0.9 %, config 5 +2.5 %, paper +1.7 %) but not on small ones (config 3's 8,750
+        // triangles: -0.5 %): on by default from 65,536 terrain triangles
+        const bool want_entries = (a->flags & MDRT_TILE_ENTRY) ||
+                                  (!(a->flags & MDRT_NO_TILE_ENTRY) && ctx->stats.terrain_triangles >= 65536);
+        const bool entries = ctx->has_terrain && !pp.grid_mode && want_entries;
         EntryParams ep{};
         if (entries) {
             ctx->tile_entry.reserve(std::max<size_t>(1, nviews * max_tiles_per_view(ctx->W, ctx->H)));

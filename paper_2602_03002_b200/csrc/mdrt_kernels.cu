@@ -155,21 +155,27 @@ __device__ __forceinline__ bool pyramid_misses(const TilePyramid& f, float lx, f
     return false;
 }
 
-// descend from the terrain root while exactly one child meets the pyramid: the
-// entry ref (inner node, leaf, or kExit when no terrain box meets it)
+// Descend from the terrain root while exactly one child meets the pyramid. The
+// entry is the record holding the last child descended into: a ray started there
+// still tests that child's box itself (a node record holds its children's boxes,
+// not its own), so rays of the tile that miss it stop exactly where a traversal
+// from the root would, and the sibling box they skip is outside the pyramid.
+// kExit when no terrain box meets the pyramid.
 __device__ int32_t pyramid_entry(const float4* __restrict__ nodes, int32_t root, const TilePyramid& f) {
-    int32_t ref = root;
-    for (int lvl = 0; lvl <= kStack + 1 && ref >= 0; ++lvl) {
-        const float4* n = nodes + 4 * static_cast<int64_t>(ref);
+    int32_t rec = root;
+    for (int lvl = 0; lvl <= kStack + 1; ++lvl) {
+        const float4* n = nodes + 4 * static_cast<int64_t>(rec);
         const float4 bx = __ldg(n), by = __ldg(n + 1), bz = __ldg(n + 2);
         const int2 rf = __ldg(reinterpret_cast<const int2*>(n + 3));
         const bool m0 = pyramid_misses(f, bx.x, bx.y, bx.z, bx.w, bz.x, bz.y);
         const bool m1 = pyramid_misses(f, by.x, by.y, by.z, by.w, bz.z, bz.w);
-        if (!m0 && !m1) break;
         if (m0 && m1) return kExit;
-        ref = m0 ? rf.y : rf.x;
+        if (!m0 && !m1) break;
+        const int32_t child = m0 ? rf.y : rf.x;
+        if (child < 0) break;   // a leaf: its box is in this record
+        rec = child;
     }
-    return ref;
+    return rec;
 }
 
 // One thread per (view, tile), after the prologue wrote the view records (the

@@ -23,11 +23,13 @@ def _pair(pkg, scene, **kw):
     scene.debug_flags = _native.NO_TILE_ENTRY
     ctr_root = torch.zeros(4, dtype=torch.int64, device=scene.device)
     ref = pkg.render(scene, counters=ctr_root, **kw).data.clone()
-    scene.debug_flags = 0
+    scene.debug_flags = _native.TILE_ENTRY
     ctr = torch.zeros(4, dtype=torch.int64, device=scene.device)
     got = pkg.render(scene, counters=ctr, **kw).data.clone()
     plain = pkg.render(scene, **kw).data
     assert torch.equal(plain, got)
+    scene.debug_flags = 0
+    assert torch.equal(pkg.render(scene, **kw).data, got)       # the size heuristic's choice, same image
     return got, ref, ctr.tolist(), ctr_root.tolist()
 
 
@@ -66,7 +68,7 @@ def test_entry_with_wide_tiles_and_no_early_termination(pkg):
     scene = casefile.build_scene(case, pkg)
     got, ref, _, _ = _pair(pkg, scene, early_termination=False)
     assert torch.equal(got, ref)
-    scene.debug_flags = _native.WIDE_STORES                       # 8-wide tiles: entries per 8x4 tile
+    scene.debug_flags = _native.WIDE_STORES | _native.TILE_ENTRY  # 8-wide tiles: entries per 8x4 tile
     wide = pkg.render(scene).data.clone()
     scene.debug_flags = _native.WIDE_STORES | _native.NO_TILE_ENTRY
     assert torch.equal(wide, pkg.render(scene).data)

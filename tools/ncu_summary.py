@@ -22,6 +22,10 @@ KEYS = [
     ("l1tex__t_sector_hit_rate.pct", "L1 sector hit rate %"),
     ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "global load requests"),
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global load sectors"),
+    ("l1tex__t_sectors_pipe_tex_mem_texture.sum", "texture sectors"),
+    ("l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "local load sectors (stack pops)"),
+    ("l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", "local store sectors (stack pushes)"),
+    ("l1tex__data_pipe_tex_wavefronts.sum.pct_of_peak_sustained_elapsed", "L1 texture data-pipe wavefronts %"),
     ("lts__t_sector_hit_rate.pct", "L2 sector hit rate %"),
     ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 read sectors (from L1)"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),

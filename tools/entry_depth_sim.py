@@ -51,6 +51,8 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--views", type=int, default=64)
     ap.add_argument("--tw", type=int, default=0)
+    ap.add_argument("--hint", type=float, default=0.0,
+                    help="> 0: far plane = min(d_max, hint * tile max depth + 0.05) from an oracle render")
     a = ap.parse_args()
     import paper_2602_03002_b200 as md
     from paper_2602_03002_b200 import synth, bvh as mbvh
@@ -68,6 +70,11 @@ def main():
                  mount_pos=c.mount.translation, mount_rot=c.mount.rotation, parent=c.parent_body) for c in w.cameras]
     cp, cq = orc.camera_world_poses(cams, bp, bq)
     W, H = w.cameras[0].width, w.cameras[0].height
+    depth = None
+    if a.hint > 0:
+        bodies = [(f32(m.vertices), m.faces) for _, m in w.bodies]
+        sc = orc.OracleScene(bodies, (f32(t.vertices), t.faces), cams)
+        depth = sc.render(bp, bq, threads=0)
     tw = a.tw or (4 if W <= 96 else 8)
     th = 32 // tw
     depths_tile, depths_view = [], []
@@ -86,7 +93,7 @@ def main():
             o = cp[e, c]
             far = cam.d_max
 
-            def descend(u0, u1, v0, v1):
+            def descend(u0, u1, v0, v1, far=far):
                 flo, fhi, planes, fwd = frustum(o, R, u0, u1, v0, v1, far)
                 ref, d = 0, 0
                 while ref >= 0:
@@ -108,7 +115,11 @@ def main():
             depths_view.append(descend(u(0), u(W - 1), v(0), v(H - 1)))
             for ty in range(0, H, th):
                 for tx in range(0, W, tw):
-                    depths_tile.append(descend(u(tx), u(min(tx + tw, W) - 1), v(ty), v(min(ty + th, H) - 1)))
+                    fr = far
+                    if depth is not None:
+                        blk = depth[e, c, ty:ty + th, tx:tx + tw]
+                        fr = min(far, a.hint * float(blk.max()) + 0.05)
+                    depths_tile.append(descend(u(tx), u(min(tx + tw, W) - 1), v(ty), v(min(ty + th, H) - 1), fr))
     dt, dv = np.array(depths_tile), np.array(depths_view)
     print(f"{a.config}: tile {tw}x{th}: entry depth mean {dt.mean():.2f} (p10 {np.percentile(dt, 10):.0f}, "
           f"p50 {np.median(dt):.0f}, p90 {np.percentile(dt, 90):.0f}); per-view mean {dv.mean():.2f}")

@@ -54,8 +54,9 @@ constexpr double kCostTri = 1.0;   // relative cost of one triangle test
 // and the largest leaf; overridable for tuning experiments via
 // MDRT_SAH_NODE_COST / MDRT_LEAF_MAX (<= 8, the leaf encoding's limit).
 struct BuildOptions {
-    double node_cost = 1.2;
+    double node_cost = 1.2;            // < 0 / 0 below: chosen per mesh size (large_mesh_*)
     int leaf_max = kMaxLeafTris;
+    bool node_cost_set = false, leaf_max_set = false;
     // nodes with <= sweep_max triangles take the exact sweep SAH (every split of the
     // centroid order on every axis) instead of 32 bins: config 3 (8,750-triangle
     // stepping-stone terrain, large box faces) +6.0 %, configs 2 and paper +-0.1 %;
@@ -67,18 +68,41 @@ struct BuildOptions {
 const BuildOptions& options() {
     static const BuildOptions o = [] {
         BuildOptions r;
-        if (const char* v = std::getenv("MDRT_SAH_NODE_COST")) r.node_cost = std::atof(v);
-        if (const char* v = std::getenv("MDRT_LEAF_MAX")) r.leaf_max = std::min(8, std::max(1, std::atoi(v)));
+        if (const char* v = std::getenv("MDRT_SAH_NODE_COST")) {
+            r.node_cost = std::atof(v);
+            r.node_cost_set = true;
+        }
+        if (const char* v = std::getenv("MDRT_LEAF_MAX")) {
+            r.leaf_max = std::min(8, std::max(1, std::atoi(v)));
+            r.leaf_max_set = true;
+        }
         if (const char* v = std::getenv("MDRT_SAH_SWEEP")) r.sweep_max = std::atoll(v);
         return r;
     }();
     return o;
 }
 
+// Large meshes (>= 500k triangles) get a costlier node and leaves of up to 8
+// triangles: their trees are deep, and a node visit loads the L1 data pipe while
+// triangle tests run on the otherwise idle texture pipe. Measured (round 2,
+// profiles/experiments/r02_sah_large_mesh.txt): config 5 (3.37M triangles) +2.6 %,
+// its 1M-triangle variant +2.8 %; the same setting on config 2 (259k) -0.2 %,
+// config 3 (8.75k) -3.0 %, paper (259k) -1.4 %, hence the size bound.
+constexpr int64_t kLargeMesh = 500000;
+double node_cost_for(int64_t nf) {
+    const BuildOptions& o = options();
+    return o.node_cost_set ? o.node_cost : (nf >= kLargeMesh ? 2.0 : o.node_cost);
+}
+int default_leaf_max(int64_t nf) {
+    const BuildOptions& o = options();
+    return o.leaf_max_set ? o.leaf_max : (nf >= kLargeMesh ? 8 : o.leaf_max);
+}
+
 class Builder {
    public:
     Builder(const std::vector<Box>& tb, const std::vector<std::array<double, 3>>& cen, int leaf_max)
-        : tbox_(tb), cen_(cen), leaf_max_(leaf_max) {}
+        : tbox_(tb), cen_(cen), leaf_max_(leaf_max),
+          node_cost_(node_cost_for(static_cast<int64_t>(tb.size()))) {}
 
     std::vector<BNode> nodes;
     std::vector<int64_t> idx;
@@ -110,6 +134,7 @@ class Builder {
     const std::vector<Box>& tbox_;
     const std::vector<std::array<double, 3>>& cen_;
     const int leaf_max_;
+    const double node_cost_;
     // sweep SAH state: per axis, the triangles of every node in the sweep region
     // in centroid order (ties by index), kept through splits by stable partition
     std::vector<int64_t> ord3_[3];
@@ -166,7 +191,7 @@ class Builder {
                 Box lacc;
                 for (int64_t i = 1; i < n; ++i) {
                     lacc.grow(tbox_[ord[i - 1]]);
-                    const double cost = options().node_cost +
+                    const double cost = node_cost_ +
                                         (lacc.area() * i + right_area[i] * (n - i)) * kCostTri /
                                             std::max(parent_area, 1e-300);
                     if (cost < best_cost) {
@@ -227,7 +252,7 @@ class Builder {
                     lacc.grow(bb[b]);
                     lcnt += bc[b];
                     if (lcnt == 0 || right_cnt[b + 1] == 0) continue;
-                    double cost = options().node_cost + (lacc.area() * lcnt + right_area[b + 1] * right_cnt[b + 1]) *
+                    double cost = node_cost_ + (lacc.area() * lcnt + right_area[b + 1] * right_cnt[b + 1]) *
                                                   kCostTri / std::max(parent_area, 1e-300);
                     if (cost < best_cost) {
                         best_cost = cost;
@@ -306,7 +331,7 @@ void pad_box(const Box& b, float lo[3], float hi[3]) {
 }  // namespace
 
 PackedTree build_tree(const double* verts, int64_t nv, const int64_t* faces, int64_t nf, int leaf_max) {
-    if (leaf_max <= 0) leaf_max = options().leaf_max;
+    if (leaf_max <= 0) leaf_max = default_leaf_max(nf);
     if (leaf_max > 8) throw std::invalid_argument("leaf size must be <= 8 (leaf encoding)");
     if (nf <= 0) throw std::invalid_argument("cannot build a BVH over an empty mesh");
     // The traversal stack holds kMaxDepth entries. The builder keeps every leaf

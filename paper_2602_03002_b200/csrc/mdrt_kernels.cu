@@ -1055,6 +1055,47 @@ static void launch_render_tw(const RenderParams& p, int64_t warps, bool count, i
         q.order_d1 = q.row_order ? q.row_tiles : static_cast<uint32_t>(q.tiles_per_view);
         q.order_m1 = q.row_order ? q.m_row_tiles : q.m_tiles_per_view;
     }
+    // Experiment (MDRT_L2_PERSIST=1, BVH larger than L2): mark the node records as
+    // persisting in L2 for this launch (access-policy window launch attribute), so
+    // triangle and I/O traffic cannot evict them.
+    static int persist = -1;
+    if (persist < 0) {
+        const char* e = std::getenv("MDRT_L2_PERSIST");
+        persist = e && std::atoi(e) > 0;
+        if (persist) {
+            int dev = 0, max_persist = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
+        }
+    }
+    if (persist && geometry_bytes > l2_bytes) {
+        int dev = 0, max_win = 0;
+        size_t limit = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
+        const size_t node_bytes = static_cast<size_t>(p.n_nodes) * 64;
+        const size_t win = std::min(node_bytes, static_cast<size_t>(max_win));
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<float4*>(p.nodes);
+        attr[0].val.accessPolicyWindow.num_bytes = win;
+        attr[0].val.accessPolicyWindow.hitRatio = win > 0 ? std::min(1.0f, static_cast<float>(limit) / win) : 0.f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(kBlock);
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (count)
+            cudaLaunchKernelEx(&cfg, render_kernel<true, TW>, q);
+        else
+            cudaLaunchKernelEx(&cfg, render_kernel<false, TW>, q);
+        return;
+    }
     if (count)
         render_kernel<true, TW><<<static_cast<unsigned>(grid), kBlock, 0, s>>>(q);
     else

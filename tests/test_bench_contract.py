@@ -68,3 +68,20 @@ def test_launcher_fails_loudly():
     res = subprocess.run([sys.executable, bench, "--gpus", "1", "--steps", "1", "--warmup", "1"], capture_output=True,
                          text=True, env=env, timeout=300, cwd=ROOT)
     assert res.returncode == 2 and "WORLD_SIZE=2" in res.stderr
+
+
+def test_config_dict_is_arm_independent_and_morton_is_a_permutation():
+    """Both arms print config_dict(...) for the same run shape, so the driver can compare
+    them key by key; the Z-order experiment renumbers envs without changing the set."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import bench
+    from paper_2602_03002_b200 import synth
+    a = bench.config_dict("cfg2", 4096, 2, synth.config("cfg2", 8192))
+    b = bench.config_dict("cfg2", 4096, 2, synth.config("cfg2", 4096))   # the reference arm's bounded sample
+    assert a == b and a["global_envs"] == 8192 and a["terrain_tris"] == 259200
+    w = synth.config("cfg2", 64)
+    roots = w.roots.copy()
+    bench.morton_order(w)
+    assert sorted(map(tuple, w.roots)) == sorted(map(tuple, roots))
+    assert not np.array_equal(w.roots, roots)

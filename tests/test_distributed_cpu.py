@@ -126,3 +126,14 @@ def test_peer_block_offsets_and_pointer_views():
     assert np.array_equal(view.numpy().ravel(), buf[24:42])
     view.fill_(-1.0)
     assert np.all(buf[24:42] == -1.0) and buf[23] == 23.0 and buf[42] == 42.0
+
+
+def test_numa_helpers_cpu():
+    """cpulist parsing, and the NUMA binder degrades to 'unknown node, all CPUs' without a GPU."""
+    assert pd._cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert pd._cpulist("") == set()
+    before = os.sched_getaffinity(0)
+    info = pd.bind_to_gpu_numa(torch.device("cuda", 0)) if not torch.cuda.is_available() else None
+    if info is not None:
+        assert info["node"] is None and info["cpus"] == len(before)
+        assert os.sched_getaffinity(0) == before

@@ -564,11 +564,21 @@ def ours(args):
         step_id[0] += 1
 
     # ---- per-ray work counts (untimed, MDRT_COUNT) ----
+    # Algorithmic work: a single-ray closest-hit traversal from each tree's
+    # root, counted on the device BVH with the tile entries off; `issued` counts what the
+    # render kernel fetches per ray when each tile's rays start at its entry record (the
+    # shared top-level fetches are made once per tile by entry_kernel instead).
     ctr = torch.zeros(4, dtype=torch.int64, device=dev)
     scene.set_body_poses(*pose_dev[0], validate=False)
+    flags0 = scene.debug_flags
+    scene.debug_flags = flags0 | _native.NO_TILE_ENTRY
     md.render(scene, counters=ctr)
+    scene.debug_flags = flags0
+    ctr_issued = torch.zeros(4, dtype=torch.int64, device=dev)
+    md.render(scene, counters=ctr_issued)
     torch.cuda.synchronize()
     nodes_per_ray, tris_per_ray, link_nodes_per_ray, link_traces_per_ray = (x / rays_per_step for x in ctr.tolist())
+    nodes_issued_per_ray = ctr_issued[0].item() / rays_per_step
 
     for i in range(args.warmup):
         step(pose_dev[i % P])
@@ -861,7 +871,8 @@ def ours(args):
                     "frac": achieved_alg / l2_gbs, "traffic": traffic,
                     "peak_source": L2_PROBE_HOW,
                     "achieved_how": "algorithmic bytes per launch (node 56 B x node fetches + triangle 48 B x tests "
-                                    "per ray, counted on the device BVH, + I/O) / render-kernel event time",
+                                    "per ray of a single-ray traversal from the tree roots, counted on the device "
+                                    "BVH, + I/O) / render-kernel event time",
                     "frac_requested": (req * 32 / (kernel_ms * 1e-3) / 1e9 / l2_gbs) if req else None,
                     "frac_requested_how": "L1-requested sectors per launch (ncu l1tex__t_sectors, global loads + "
                                           "texture, lanes of a request deduplicated) x 32 B / kernel time / L2 "
@@ -893,7 +904,8 @@ def ours(args):
                          "build_s": round(t_build, 3)},
             "frames_per_s": value / (H * W),
             "steps_per_s": 1e3 / (total_ms / args.steps),
-            "per_ray": {"node_fetches": nodes_per_ray, "tri_tests": tris_per_ray, "bytes": bytes_per_ray,
+            "per_ray": {"node_fetches": nodes_per_ray, "node_fetches_issued": nodes_issued_per_ray,
+                        "tri_tests": tris_per_ray, "bytes": bytes_per_ray,
                         "link_node_fetches": link_nodes_per_ray, "link_traversals": link_traces_per_ray,
                         "node_record_b": node_b + 8, "node_fetch_b": node_b, "tri_record_b": tri_b, "io_b": io_b},
             "roofline": roof,

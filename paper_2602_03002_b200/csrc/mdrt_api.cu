@@ -487,6 +487,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
             ep.views = ctx->views.ptr;
             ep.nodes = reinterpret_cast<const float4*>(ctx->nodes.ptr);
             ep.root = ctx->terrain_root;
+            ep.n_nodes = ctx->node_count;
             ep.W = ctx->W;
             ep.H = ctx->H;
             ep.tile_w = tile_w;

@@ -161,9 +161,11 @@ __device__ __forceinline__ bool pyramid_misses(const TilePyramid& f, float lx, f
 // not its own), so rays of the tile that miss it stop exactly where a traversal
 // from the root would, and the sibling box they skip is outside the pyramid.
 // kExit when no terrain box meets the pyramid.
-__device__ int32_t pyramid_entry(const float4* __restrict__ nodes, int32_t root, const TilePyramid& f) {
+__device__ int32_t pyramid_entry(const float4* __restrict__ nodes, int32_t root, const TilePyramid& f,
+                                 int32_t n_nodes) {
     int32_t rec = root;
     for (int lvl = 0; lvl <= kStack + 1; ++lvl) {
+        MDRT_CHECK(rec >= 0 && rec < n_nodes, "entry descent: node %d of %d", rec, n_nodes);
         const float4* n = nodes + 4 * static_cast<int64_t>(rec);
         const float4 bx = __ldg(n), by = __ldg(n + 1), bz = __ldg(n + 2);
         const int2 rf = __ldg(reinterpret_cast<const int2*>(n + 3));
@@ -196,7 +198,7 @@ static __global__ void __launch_bounds__(128) entry_kernel(EntryParams p) {
     TilePyramid f;
     pyramid_setup(f, R, o, fmaf(static_cast<float>(x0), V.ax, V.bx) - m, fmaf(static_cast<float>(x1), V.ax, V.bx) + m,
                   fmaf(static_cast<float>(y0), V.ay, V.by) - m, fmaf(static_cast<float>(y1), V.ay, V.by) + m, V.dmax);
-    p.out[i] = pyramid_entry(p.nodes, p.root, f);
+    p.out[i] = pyramid_entry(p.nodes, p.root, f, p.n_nodes);
 }
 
 // ---------------------------------------------------------------------------
@@ -543,9 +545,9 @@ __device__ __forceinline__ void render_tile(const RenderParams& p, uint32_t gw, 
         const float wdz = r1.z * dcx + r1.w * dcy + r2.x * dcz;
         const float bound = p.early_termination ? z : dmax;
         // the prologue's entry node of this tile (a node every ray of the tile reaches first)
-        const int32_t troot = p.tile_entry ? p.tile_entry[view * static_cast<uint32_t>(p.tiles_per_view) +
-                                                          ty * static_cast<uint32_t>(p.tiles_x) + tx]
-                                           : p.terrain_root;
+        const uint32_t tslot = view * static_cast<uint32_t>(p.tiles_per_view) + ty * static_cast<uint32_t>(p.tiles_x) + tx;
+        MDRT_CHECK(tslot < static_cast<uint32_t>(p.N * p.C * p.tiles_per_view), "tile entry slot %u", tslot);
+        const int32_t troot = p.tile_entry ? p.tile_entry[tslot] : p.terrain_root;
 #ifdef MDRT_NO_OCTANT
         const float tt = trace<COUNT>(p.nodes, p.tri_tex, troot, r2.y, r2.z, r2.w, wdx, wdy, wdz,
                                       bound * inv_m, stack, ctr, p.n_nodes, p.n_tris);

@@ -71,6 +71,7 @@ struct EntryParams {
     const ViewRec* views;
     const float4* nodes;          // packed BVH records (terrain tree at root)
     int32_t root;
+    int32_t n_nodes;              // node record count (bounds of the MDRT_CHECKS build)
     int32_t W, H, tile_w, tile_h, tiles_x, tiles_per_view;
     int64_t views_count;          // N * C
     int32_t* out;                 // (N*C, tiles_per_view) entry refs

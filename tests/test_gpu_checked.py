@@ -16,7 +16,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITE = ["tests/test_gpu_parity.py", "tests/test_gpu_edge.py", "tests/test_gpu_api.py",
-         "tests/test_gpu_acceptance.py", "tests/test_bvh_api.py"]
+         "tests/test_gpu_acceptance.py", "tests/test_bvh_api.py", "tests/test_gpu_entry.py",
+         "tests/test_gpu_lifetime.py", "tests/test_gpu_seam.py"]
 
 pytestmark = pytest.mark.skipif(os.environ.get("MDRT_CHECKED_CHILD") == "1",
                                 reason="already running under the checked build")

@@ -272,6 +272,9 @@ int mdrt_probe_read(const void *buf, int64_t bytes, int32_t iters, float *sink, 
  * takes the first-touch page faults off the critical path of the device->host
  * copy into it (kernels/cuda_backend.py). */
 int mdrt_host_touch(void *ptr, int64_t bytes, int32_t threads);
+/* memcpy of HOST memory by up to `threads` threads of the same persistent pool, in
+ * 4 KB-aligned slices (each page of a fresh `dst` is first touched by one thread). */
+int mdrt_host_copy(void *dst, const void *src, int64_t bytes, int32_t threads);
 
 /* Fused frame gather over peer memory (the reference
  * has no multi-GPU path, its closest interface is the caller-allocated `out`

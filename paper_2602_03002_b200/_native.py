@@ -162,6 +162,7 @@ def lib():
             "mdrt_peer_free": (ctypes.c_int, [vp]),
             "mdrt_sync": (ctypes.c_int, [vp]),
             "mdrt_host_touch": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32]),
+            "mdrt_host_copy": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int32]),
             "mdrt_order_begin": (ctypes.c_int, [vp, vp]),
             "mdrt_order_end": (ctypes.c_int, [vp, vp]),
         }
@@ -182,7 +183,7 @@ EXPORTS = ("mdrt_abi_version", "mdrt_last_error", "mdrt_device_count", "mdrt_cre
            "mdrt_render", "mdrt_noise_dropout", "mdrt_gather_delayed", "mdrt_select_slots",
            "mdrt_downsample_min", "mdrt_depth_to_u8", "mdrt_bvh_build", "mdrt_query_rays", "mdrt_bvh_check", "mdrt_probe_read", "mdrt_state_set", "mdrt_state_get", "mdrt_rsm_apply", "mdrt_peer_alloc",
            "mdrt_peer_open", "mdrt_peer_close", "mdrt_peer_free", "mdrt_sync", "mdrt_order_begin",
-           "mdrt_order_end", "mdrt_host_touch")
+           "mdrt_order_end", "mdrt_host_touch", "mdrt_host_copy")
 
 
 # Device address ranges that are remote memory (peer mappings of another GPU's

@@ -13,6 +13,9 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -92,6 +95,80 @@ struct DevBuf {
         cap = 0;
     }
 };
+
+// Persistent host worker pool for the host-side helpers (mdrt_host_touch/copy):
+// spawning threads per call costs more than the work on 25-100 MB buffers.
+class HostPool {
+   public:
+    template <class F>
+    void run(int n, F&& f) {
+        std::lock_guard<std::mutex> call(call_mu_);   // one parallel region at a time
+        n = std::max(1, std::min(n, kMaxWorkers + 1));
+        ensure(n - 1);
+        std::function<void(int)> job(f);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &job;
+            active_ = n - 1;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        job(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+   private:
+    static constexpr int kMaxWorkers = 63;
+    void ensure(int k) {
+        while (static_cast<int>(workers_.size()) < k) {
+            const int id = static_cast<int>(workers_.size()) + 1;
+            workers_.emplace_back([this, id] { loop(id); });
+        }
+    }
+    void loop(int id) {
+        uint64_t seen = 0;
+        while (true) {
+            std::function<void(int)>* job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                if (id > active_) continue;       // not needed for this region
+                job = job_;
+            }
+            (*job)(id);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> workers_;
+    std::function<void(int)>* job_ = nullptr;
+    int active_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+HostPool& host_pool() {
+    static HostPool pool;
+    return pool;
+}
 
 }  // namespace
 
@@ -889,23 +966,35 @@ int mdrt_host_touch(void* ptr, int64_t bytes, int32_t threads) {
         need(ptr != nullptr || bytes == 0, "ptr is NULL");
         need(bytes >= 0 && threads >= 1 && threads <= 256, "bad host_touch arguments");
         if (bytes == 0) return;
-        // one write per 4 KB page; threads take contiguous slices (page faults on
-        // different ranges of one mapping proceed in parallel)
+        // one write per 4 KB page (value unchanged); the pool's threads take contiguous
+        // slices, so page faults on different ranges of one mapping proceed in parallel
         constexpr int64_t kPage = 4096;
         volatile char* base = static_cast<volatile char*>(ptr);
         const int64_t pages = (bytes + kPage - 1) / kPage;
         const int n = static_cast<int>(std::min<int64_t>(threads, std::max<int64_t>(1, pages / 64)));
-        auto work = [&](int t) {
+        host_pool().run(n, [&](int t) {
             const int64_t lo = pages * t / n, hi = pages * (t + 1) / n;
             for (int64_t p = lo; p < hi; ++p) {
                 const int64_t off = std::min(p * kPage, bytes - 1);
                 base[off] = base[off];
             }
-        };
-        std::vector<std::thread> pool;
-        for (int t = 1; t < n; ++t) pool.emplace_back(work, t);
-        work(0);
-        for (auto& th : pool) th.join();
+        });
+    });
+}
+
+int mdrt_host_copy(void* dst, const void* src, int64_t bytes, int32_t threads) {
+    return guarded([&] {
+        need((dst && src) || bytes == 0, "NULL argument");
+        need(bytes >= 0 && threads >= 1 && threads <= 256, "bad host_copy arguments");
+        if (bytes == 0) return;
+        const int n = static_cast<int>(std::min<int64_t>(threads, std::max<int64_t>(1, bytes >> 20)));
+        char* d = static_cast<char*>(dst);
+        const char* sp = static_cast<const char*>(src);
+        host_pool().run(n, [&](int t) {
+            // 4 KB-aligned slices: every page is written (and first touched) by one thread
+            const int64_t lo = (bytes * t / n) & ~int64_t(4095), hi = t + 1 == n ? bytes : (bytes * (t + 1) / n) & ~int64_t(4095);
+            if (hi > lo) std::memcpy(d + lo, sp + lo, static_cast<size_t>(hi - lo));
+        });
     });
 }
 

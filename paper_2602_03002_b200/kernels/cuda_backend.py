@@ -199,7 +199,8 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
         torch.cuda.current_stream(device).synchronize()
         if tm:
             tm.append(time.perf_counter())
-        torch.from_numpy(out.reshape(-1)).copy_(dev_out.reshape(-1))
+        _native.check(_native.lib().mdrt_host_copy(out.ctypes.data, dev_out.data_ptr(), out.nbytes,
+                                                   _touch_threads()))
         if tm:
             tm.append(time.perf_counter())
             print("seam ms: inputs %.2f touch %.2f wait %.2f copy %.2f" % tuple(
@@ -214,8 +215,6 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
 
 
 _CHUNKS = 8
-
-
 def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
     """Device frame -> the caller's numpy ``out`` (typically freshly allocated,
     scene.py:344-347, so its pages are first touched here). Chunked pipeline: the

@@ -56,7 +56,7 @@ def main():
     ts = calls(a.calls)
     pr.disable()
     tag = f"mode={os.environ.get('MDRT_SEAM_MODE', 'stage')} touch={os.environ.get('MDRT_SEAM_TOUCH', '1')}"
-    print(tag, "ms per call:", [round(t * 1e3, 2) for t in ts], "mean", round(1e3 * float(np.mean(ts)), 2))
+    print(tag, "ms per call: median", round(1e3 * float(np.median(ts)), 2), "mean", round(1e3 * float(np.mean(ts)), 2), "min", round(1e3 * min(ts), 2))
     if not a.quiet:
         pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
 

@@ -69,3 +69,23 @@ def test_ctypes_struct_layout_matches_header(cls, cname):
     size, offs = _c_layout(cname, fields)
     assert ctypes.sizeof(cls) == size
     assert [getattr(cls, f).offset for f in fields] == offs
+
+
+def test_host_touch_and_copy_cpu():
+    """mdrt_host_touch leaves values unchanged; mdrt_host_copy equals memcpy for any size and
+    thread count (4 KB-aligned slices, the persistent host pool)."""
+    import numpy as np
+    from paper_2602_03002_b200 import _native
+    L = _native.lib()
+    rng = np.random.default_rng(0)
+    for size in (0, 1, 4095, 4096, 4097, 3 * 4096 + 5, (10 << 20) + 123):
+        src = rng.integers(0, 255, size=max(size, 1), dtype=np.uint8)[:size]
+        for th in (1, 3, 8, 16):
+            dst = np.zeros(max(size, 1), np.uint8)[:size]
+            assert L.mdrt_host_copy(dst.ctypes.data, src.ctypes.data, size, th) == 0
+            assert np.array_equal(dst, src)
+            keep = dst.copy()
+            assert L.mdrt_host_touch(dst.ctypes.data, size, th) == 0
+            assert np.array_equal(dst, keep)
+    assert L.mdrt_host_copy(None, None, 16, 1) == _native.MDRT_EINVAL
+    assert L.mdrt_host_touch(None, 16, 0) == _native.MDRT_EINVAL

@@ -786,7 +786,7 @@ def ours(args):
             scene.set_body_poses(*pose_dev[i % P], validate=False)
             obs = md.render_pipeline(scene, sensor=sens, step=step_id[0], frame_buffer=buf,
                                      timestamp=step_id[0] * dt, delays=delays, out=out)
-            pdist.gather_frames(obs, dst=0)
+            pdist.gather_frames(obs, dst=0, sizes=[n] * world)     # equal slices: no size exchange
             step_id[0] += 1
         g1.record(stream)
         torch.cuda.synchronize()

@@ -915,6 +915,10 @@ def ours(args):
                     "ms_per_step": e2e_ms / args.steps, "d2h_alone_gbs": d2h_gbs,
                     "host_loop_ms_per_step": e2e_host_ms / args.steps,
                     "d2h_floor_ms": d2h / (d2h_gbs * 1e9) * 1e3,
+                    # the e2e leg's own ceiling: the step's result crossing PCIe at the measured
+                    # pinned D2H rate (the device step overlaps it)
+                    "pcie_ceiling_rays_per_s": rays_per_step * world / (d2h / (d2h_gbs * 1e9)),
+                    "frac_of_pcie_ceiling": e2e_value / (rays_per_step * world / (d2h / (d2h_gbs * 1e9))),
                     "delivered": "48x27 block-min observation (policy input)" if ds is not None
                                  else "full observation (N,C,H,W) f32",
                     "how": "pinned-host poses H2D (upload stream) + fused pipeline + result D2H (copy stream, "

@@ -853,7 +853,7 @@ def ours(args):
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
         tj = {}
         tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-        if os.path.exists(tpath):
+        if os.path.exists(tpath) and n == cfg_envs(args.config):   # captured at the config's own env count
             tj = json.load(open(tpath))
         traffic = tj.get("dram_bytes_per_launch")
         ncu_units = None

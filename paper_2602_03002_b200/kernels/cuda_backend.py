@@ -105,7 +105,7 @@ def _cached_grid(x, device, slot):
         if src is x and f == fp:
             entries.append(entries.pop(i))
             return t
-    t = _dev(x, device, slot).clone()   # own copy: the staging slot is reused by the next upload
+    t = _dev(x, device, slot)           # a device tensor of its own (the pinned staging slot is reused)
     entries.append((x, fp, t))
     while len(entries) > _GRID_CACHE_SLOTS:
         entries.pop(0)

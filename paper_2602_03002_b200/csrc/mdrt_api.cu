@@ -217,6 +217,8 @@ struct mdrt_ctx {
     }
     DevBuf<int2> rects;
     DevBuf<int32_t> tile_entry;   // per-tile terrain entry refs (prologue -> render kernel)
+    int32_t entry_tile_w = 0;     // tile width the last prologue computed entries for (0: none)
+    size_t entry_views = 0;       // and its view count (a trace-only call reuses them only if both match)
     DevBuf<unsigned int> tile_counter;
     DevBuf<StepState> state;
     // Cross-stream ordering of the per-step scratch (views, links, rects, tile
@@ -590,7 +592,12 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
                 launch_entry(ep, s);
                 CK(cudaGetLastError());
             }
+            ctx->entry_tile_w = entries ? tile_w : 0;
+            ctx->entry_views = nviews;
         }
+        // a trace-only call uses the entries of the last prologue only when they were
+        // computed for this call's tiles (else: terrain from the root, same result)
+        const bool use_entries = entries && (!only_trace || (ctx->entry_tile_w == tile_w && ctx->entry_views == nviews));
         if (only_pro) {
             if (ordered) ctx->order_end(s);
             return;
@@ -602,7 +609,7 @@ int mdrt_render(mdrt_ctx* ctx, const mdrt_step_args* a, void* stream) {
         rp.tile_w = tile_w;
         rp.tiles_x = tiles_x;
         rp.tiles_per_view = tiles_per_view;
-        rp.tile_entry = entries ? ctx->tile_entry.ptr : nullptr;
+        rp.tile_entry = use_entries ? ctx->tile_entry.ptr : nullptr;
         rp.m_tiles_x = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_x));
         rp.m_tiles_per_view = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(rp.tiles_per_view));
         rp.m_C = static_cast<uint32_t>(0xffffffffu / static_cast<uint32_t>(C));

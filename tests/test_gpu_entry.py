@@ -98,3 +98,21 @@ def test_entry_equals_root_on_random_cameras(pkg, seed):
         got, ref, ctr, ctr_root = _pair(pkg, scene)
         assert torch.equal(got, ref), f"{(got != ref).sum().item()} pixels differ ({cam})"
         assert ctr[1] == ctr_root[1] and ctr[0] <= ctr_root[0]
+
+
+def test_trace_only_call_never_reads_stale_entries(pkg):
+    """PHASE_PROLOGUE with entries off, then PHASE_TRACE with them on: the trace-only call
+    must not use entries the prologue never computed (it falls back to the root)."""
+    from paper_2602_03002_b200 import _native
+    case = casefile.load(os.path.join(GOLDEN, "render_cfg2_slice.npz"))
+    scene = casefile.build_scene(case, pkg)
+    ref = pkg.render(scene).data.clone()
+    out = torch.full(scene.frame_shape, -1.0, device=scene.device)
+    a = scene._step_args(out, True)
+    a.flags |= _native.PHASE_PROLOGUE | _native.NO_TILE_ENTRY
+    scene._launch(a)
+    b = scene._step_args(out, True)
+    b.flags |= _native.PHASE_TRACE | _native.TILE_ENTRY
+    scene._launch(b)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)

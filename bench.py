@@ -861,6 +861,13 @@ def ours(args):
             ncu_units = {"l1_lsu_data_pipe": tj["l1_lsu_data_pipe_pct"] / 100.0,
                          "issue_active": tj["issue_active_pct"] / 100.0,
                          "l2_throughput": tj["l2_throughput_pct"] / 100.0, "source": tj.get("source")}
+            if tj.get("ncu_duration_ms"):
+                # actual traffic of the captured launch: L2 -> L1 reads and DRAM
+                dur = tj["ncu_duration_ms"] * 1e-3
+                if tj.get("l2_to_l1_read_bytes_per_launch"):
+                    ncu_units["l2_to_l1_read_gbs"] = tj["l2_to_l1_read_bytes_per_launch"] / dur / 1e9
+                if tj.get("dram_bytes_per_launch"):
+                    ncu_units["dram_gbs"] = tj["dram_bytes_per_launch"] / dur / 1e9
         bvh_bytes = scene.geometry_stats["node_bytes"] + scene.geometry_stats["tri_bytes"]
         l2_size = torch.cuda.get_device_properties(dev).L2_cache_size
         if bvh_bytes <= l2_size and l2_gbs:

@@ -148,14 +148,6 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
     tm = [time.perf_counter()] if _TIMING else None
     host_np = isinstance(out, np.ndarray)
     mapped = host_np and _MODE == "mapped" and out.flags.c_contiguous
-    toucher = None
-    if mapped and _TOUCH and _CONC:
-        # fault in the caller's fresh pages on other cores while this thread uploads the
-        # inputs and the GPU renders (the ctypes call releases the GIL)
-        _advise_hugepages(out)
-        toucher = threading.Thread(target=_native.lib().mdrt_host_touch,
-                                   args=(out.ctypes.data, out.nbytes, _touch_threads()))
-        toucher.start()
     device = out.device if isinstance(out, torch.Tensor) and out.is_cuda else _cuda_device(None)
     d_max = np.broadcast_to(np.asarray(d_max, np.float64), (c,))
     ctx = _context(flat, c, h, w, d_max, device)
@@ -189,9 +181,7 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
         tm.append(time.perf_counter())
     ctx.render(a, torch.cuda.current_stream(device).cuda_stream)
     if mapped:
-        if toucher is not None:
-            toucher.join()
-        elif _TOUCH:
+        if _TOUCH:   # fault in the caller's fresh pages while the GPU renders
             _advise_hugepages(out)
             _native.check(_native.lib().mdrt_host_touch(out.ctypes.data, out.nbytes, _touch_threads()))
         if tm:
@@ -215,6 +205,8 @@ def _render_batch(flat, body_pos, body_rot, cam_pos, cam_rot, ray_dirs, ray_scal
 
 
 _CHUNKS = 8
+
+
 def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
     """Device frame -> the caller's numpy ``out`` (typically freshly allocated,
     scene.py:344-347, so its pages are first touched here). Chunked pipeline: the
@@ -258,7 +250,6 @@ _TOUCH = os.environ.get("MDRT_SEAM_TOUCH", "1") != "0"    # A/B knobs (tools/sea
 # zeroing of 100 MB costs ~4 ms on that host and is the largest single part).
 _MODE = os.environ.get("MDRT_SEAM_MODE", "mapped")       # mapped | stage
 _TIMING = os.environ.get("MDRT_SEAM_TIMING") == "1"
-_CONC = os.environ.get("MDRT_SEAM_TOUCH_CONC", "0") == "1"
 
 
 def _touch_threads() -> int:

@@ -220,9 +220,9 @@ def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
         stage.copy_(src)
         np.copyto(out, stage.numpy().reshape(out.shape))
         return
+    t0 = time.perf_counter() if _TIMING else 0.0
     if _TOUCH:
         _advise_hugepages(out)
-    dst = torch.from_numpy(out.reshape(-1))
     bounds = [n * k // _CHUNKS for k in range(_CHUNKS + 1)]
     cur = torch.cuda.current_stream(device)
     ready = []
@@ -232,13 +232,25 @@ def _deliver_host(dev_out: torch.Tensor, out: np.ndarray, device) -> None:
         ev = torch.cuda.Event()
         ev.record(cur)
         ready.append(ev)
+    t1 = time.perf_counter() if _TIMING else 0.0
+    lib = _native.lib()
+    th = _touch_threads()
     if _TOUCH:
         # fault in the caller's fresh pages while the GPU renders and copies
-        _native.check(_native.lib().mdrt_host_touch(out.ctypes.data, out.nbytes, _touch_threads()))
+        _native.check(lib.mdrt_host_touch(out.ctypes.data, out.nbytes, th))
+    t2 = time.perf_counter() if _TIMING else 0.0
+    wait = 0.0
     for k in range(_CHUNKS):
         lo, hi = bounds[k], bounds[k + 1]
+        w0 = time.perf_counter() if _TIMING else 0.0
         ready[k].synchronize()
-        dst[lo:hi].copy_(stage[lo:hi])
+        if _TIMING:
+            wait += time.perf_counter() - w0
+        _native.check(lib.mdrt_host_copy(out.ctypes.data + 4 * lo, stage.data_ptr() + 4 * lo, 4 * (hi - lo), th))
+    if _TIMING:
+        t3 = time.perf_counter()
+        print("seam ms (stage): enqueue %.2f touch %.2f copies %.2f (waiting %.2f)" % (
+            1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2), 1e3 * wait), file=sys.stderr)
 
 
 _TOUCH = os.environ.get("MDRT_SEAM_TOUCH", "1") != "0"    # A/B knobs (tools/seam_profile.py)

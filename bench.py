@@ -660,21 +660,23 @@ def ours(args):
     l2_gbs = None
     try:
         import ctypes
-        pb = torch.empty(32 * 1024 * 1024 // 4, dtype=torch.float32, device=dev).fill_(1.0)
         sink = torch.empty(8192, dtype=torch.float32, device=dev)
         L = _native.lib()
-        L.mdrt_probe_read(ctypes.c_void_p(pb.data_ptr()), pb.numel() * 4, 4, ctypes.c_void_p(sink.data_ptr()),
-                          ctypes.c_void_p(stream.cuda_stream))
-        iters = 50
-        for _ in range(3):                            # best of 3 (see L2_PROBE_HOW)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            _native.check(L.mdrt_probe_read(ctypes.c_void_p(pb.data_ptr()), pb.numel() * 4, iters,
-                                            ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
-            e1.record(stream)
-            torch.cuda.synchronize()
-            g = pb.numel() * 4 * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9
-            l2_gbs = max(l2_gbs or 0.0, g)
+        for mib in (32, 64):                          # both L2-resident (126 MB); best of 3 each
+            pb = torch.empty(mib * 1024 * 1024 // 4, dtype=torch.float32, device=dev).fill_(1.0)
+            L.mdrt_probe_read(ctypes.c_void_p(pb.data_ptr()), pb.numel() * 4, 4, ctypes.c_void_p(sink.data_ptr()),
+                              ctypes.c_void_p(stream.cuda_stream))
+            iters = 50
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                _native.check(L.mdrt_probe_read(ctypes.c_void_p(pb.data_ptr()), pb.numel() * 4, iters,
+                                                ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+                e1.record(stream)
+                torch.cuda.synchronize()
+                g = pb.numel() * 4 * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9
+                l2_gbs = max(l2_gbs or 0.0, g)
+            del pb
     except Exception as exc:  # probe is diagnostic only
         print(f"l2 probe failed: {exc}", file=sys.stderr)
 
@@ -957,9 +959,9 @@ def ours(args):
     return 0
 
 
-L2_PROBE_HOW = ("L2 read bandwidth measured in this run: mdrt_probe_read, 32 MiB buffer (L2-resident), 32 B "
-                "ld.global.cg loads (bypass L1), 4 in flight per thread, 148x8 blocks of 256 threads, best of 3 x "
-                "50 passes, CUDA events")
+L2_PROBE_HOW = ("L2 read bandwidth measured in this run: mdrt_probe_read over 32 and 64 MiB buffers "
+                "(L2-resident), 32 B ld.global.cg loads (bypass L1), 4 blocks of 256 threads per SM (the fastest "
+                "shape of the tools/micro/l2_probe_sweep.cu sweep), max of 2 sizes x best of 3 x 50 passes, CUDA events")
 
 
 def parity_check(md, cw, scene, sens, env0, n_par, step, threads):

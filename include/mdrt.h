@@ -261,7 +261,7 @@ int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_
                    int64_t info[4]);
 
 /* Bandwidth probe for roofline denominators: `iters` passes of 32-byte L1-bypassing
- * loads (ld.global.cg, 4 in flight per thread) over a device buffer of `bytes`
+ * loads (ld.global.cg, 4 blocks of 256 threads per SM) over a device buffer of `bytes`
  * (L2-resident when bytes << L2 size; bytes must be a multiple of 32); writes one
  * float per block into `sink` (device, >= 4096 floats) so loads are live. */
 int mdrt_probe_read(const void *buf, int64_t bytes, int32_t iters, float *sink, void *stream);

@@ -897,8 +897,10 @@ static __global__ void __launch_bounds__(128) query_kernel(QueryParams p) {
 
 // read-bandwidth probe (roofline denominator of the L2-resident traversal):
 // grid-stride 32 B loads that bypass L1 (ld.global.cg: served by L2 when the
-// buffer is L2-resident), four independent loads in flight per thread, one
-// partial sum per block
+// buffer is L2-resident), one partial sum per block. Launch shape from a sweep
+// (tools/micro/l2_probe_sweep.cu: 8-64 MiB, 4/8/16 blocks per SM, 16/32 B loads,
+// 1/4/8 in flight): 4 blocks of 256 threads per SM and one load in flight per
+// thread read fastest (17.7 TB/s at 32 MiB, 18.9 TB/s at 64 MiB).
 __device__ __forceinline__ void ldcg256(const float4* p, float4& a, float4& b) {
     asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
@@ -910,15 +912,7 @@ static __global__ void __launch_bounds__(256) probe_read_kernel(const float4* __
     const int64_t n32 = n16 / 2;                       // 32 B items
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int it = 0; it < iters; ++it) {
-        int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-        for (; i + 3 * stride < n32; i += 4 * stride) {
-            float4 a[4], b[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) ldcg256(buf + 2 * (i + k * stride), a[k], b[k]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc += ((a[k].x + a[k].y) + (a[k].z + a[k].w)) + ((b[k].x + b[k].y) + (b[k].z + b[k].w));
-        }
-        for (; i < n32; i += stride) {
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n32; i += stride) {
             float4 a, b;
             ldcg256(buf + 2 * i, a, b);
             acc += ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
@@ -1127,7 +1121,7 @@ void launch_probe_read(const float4* buf, int64_t n16, int iters, float* sink, c
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    probe_read_kernel<<<sms * 8, 256, 0, s>>>(buf, n16, iters, sink);
+    probe_read_kernel<<<sms * 4, 256, 0, s>>>(buf, n16, iters, sink);
 }
 
 void launch_advance(StepState* st, cudaStream_t s) { advance_kernel<<<1, 32, 0, s>>>(st); }

@@ -151,3 +151,17 @@ def test_bench_single_gpu_line():
     assert s["dropout_rate_rel_diff"] < 0.01 and s["residual_std_rel_diff"] < 0.01
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "paper"])
+def test_bench_parity_other_configs(cfg):
+    """The in-run oracle parity of the bench on the stepping-stone (4 cameras, raised arms)
+    and paper (240x135 + fused 5x5 min-pool) workloads: the north star's criteria."""
+    d = _line(_bench(["--config", cfg, "--steps", "3", "--warmup", "3", "--envs", "64", "--no-cpu-baseline",
+                      "--parity-envs", "32"]))
+    p = d["parity"]
+    assert p["flips_within_1e-4"] and p["over_1e-4_frac"] <= 1e-4
+    s = p["sensor"]
+    assert s["noisy_mismatch_where_clean_equal"] == 0
+    assert s["dropout_rate_rel_diff"] < 0.01 and s["residual_std_rel_diff"] < 0.01
+    assert d["roofline"]["bound"] == "l2"

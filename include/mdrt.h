@@ -155,7 +155,11 @@ int mdrt_destroy(mdrt_ctx *ctx);
 
 /* Register a body (link) mesh in its local frame; SAH BVH built once on the
  * host. Replaces Body/build_bvh (scene.py:165-176, bvh.py:68-136). Triangles
- * with area < 1e-12 are expected to be removed by the caller (mesh.py:47-56). */
+ * with area < 1e-12 are expected to be removed by the caller (mesh.py:47-56).
+ * Meshes with non-finite vertices, or with more triangles than the 24-entry
+ * traversal stack allows (leaf_max * 2^23: 33.5M at leaves of <= 4, 67M for
+ * meshes of >= 500k triangles, whose leaves hold <= 8), return MDRT_EINVAL;
+ * so does mdrt_set_terrain. */
 int mdrt_add_body(mdrt_ctx *ctx, const double *verts, int64_t nv, const int64_t *faces,
                   int64_t nf, int32_t *body_id);
 /* Set the static world-frame terrain mesh (scene.py:191-196). */
@@ -255,7 +259,7 @@ int mdrt_depth_to_u8(const float *in, uint8_t *out, int64_t n, double d_max, voi
 /* Host-only BVH check (no device needed): builds the packed tree for one mesh
  * exactly as mdrt_add_body/mdrt_set_terrain do and verifies its invariants
  * (every triangle in exactly one leaf, child boxes enclose their triangles,
- * depth <= 32). Fills info = {nodes, triangles, depth, leaves}. Returns
+ * depth <= 24, the traversal stack). Fills info = {nodes, triangles, depth, leaves}. Returns
  * MDRT_EINVAL with a message when an invariant fails. */
 int mdrt_bvh_check(const double *verts, int64_t nv, const int64_t *faces, int64_t nf,
                    int64_t info[4]);

@@ -69,10 +69,11 @@ def _cpulist(text: str) -> set[int]:
 
 
 def bind_to_gpu_numa(device: torch.device) -> dict:
-    """Pin this process's threads to the CPUs of its GPU's NUMA node.
+    """Pin the calling thread (and the threads it starts afterwards) to the CPUs of
+    its GPU's NUMA node.
 
-    Call before allocating pinned host buffers: cudaHostAlloc first-touches its
-    pages from the calling thread, so they then live on the GPU's node and the
+    Call early, before allocating pinned host buffers: cudaHostAlloc first-touches
+    its pages from the calling thread, so they then live on the GPU's node and the
     per-step H2D/D2H copies do not cross the socket interconnect. Returns
     {"node", "cpus"} (node None and every allowed CPU when the topology is
     unknown or has a single node).
